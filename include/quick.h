@@ -1,0 +1,109 @@
+/*
+ * quick.h -- C-ABI of libquick.so, a B200 (sm_100a) implementation of the QUICK W4A16 path.
+ *
+ * The operation (PAPER.md = arXiv 2402.10076, "P:L<n>" = its line n):
+ *   Y[M][N] = X[M][K] . dequant(Wq)[K][N],   dequant(q)[k][n] = (q[k][n] - z[k/G][n]) * s[k/G][n]
+ *   "mixed precision GEMM" with fp16 activations and 4-bit weights (§2.3, §4);
+ *   weights are "interleaved ... offline" (abstract P:L10; §3; §3.2) so the
+ *   kernel never writes dequantized weights back to shared memory (Fig. 2).
+ *
+ * Conventions shared by every entry point:
+ *   - Plain C types only; no C++ types or exceptions cross this boundary.  All calls are
+ *     thread-safe.  The library keeps no pointer after a call returns; the caller owns and
+ *     frees every buffer.
+ *   - Errors are returned as quick_status_t, never printed.  Device-side faults surface
+ *     asynchronously, per CUDA convention, on the stream the call was issued to.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - AWQ "GEMM" checkpoint format (reading R2): qweight uint32 [K][N/8], nibble i
+ *     (bits 4i..4i+3) of qweight[k][j] holds the code of column 8j + {0,2,4,6,1,3,5,7}[i];
+ *     zeros uint32 [K/G][N/8] packed the same way; scales fp16 bits uint16 [K/G][N].
+ *   - Supported shapes (layout v1): K % 64 == 0, N % 128 == 0, G in {32, 64, 128, 256, ...}
+ *     with K % G == 0 and G % 32 == 0.  Other shapes return QUICK_ERR_UNSUPPORTED; invalid
+ *     arguments (null pointers, negative sizes) return QUICK_ERR_INVALID_ARG.
+ */
+#ifndef QUICK_H_
+#define QUICK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QUICK_OK = 0,
+  QUICK_ERR_INVALID_ARG = 1, /* null pointer, M/N/K/G <= 0 (M < 0), bad ld, K % G != 0 */
+  QUICK_ERR_UNSUPPORTED = 2, /* N % 128, K % 64, G % 32 != 0; misaligned pointer; bad override */
+  QUICK_ERR_CUDA = 3         /* CUDA runtime/driver error; see quick_last_cuda_error()        */
+} quick_status_t;
+
+/* Version of the packed layout produced by quick_pack_weights (v1). */
+uint32_t quick_layout_version(void);
+
+/* Bytes of the packed blob for (K, N, G): K*N/2 weight bytes + (K/G)*N*2.5 metadata bytes
+ * (fp16 scale + 4-bit zero per (group, column)).  Returns 0 if the shape is unsupported. */
+size_t quick_packed_bytes(int K, int N, int group_size);
+
+/* Offline repack (host; §3.2, Figs. 4-6): AWQ tensors -> v1 blob.
+ *   qweight  host, uint32 [K][N/8], AWQ order
+ *   scales   host, uint16 [K/G][N], fp16 bit patterns (copied verbatim, incl. NaN/Inf)
+ *   zeros    host, uint32 [K/G][N/8], AWQ order
+ *   packed_out host, quick_packed_bytes(K, N, G) bytes, written completely.
+ * Deterministic pure function of its inputs; bit-exact and invertible (quick_unpack_weights). */
+quick_status_t quick_pack_weights(const uint32_t* qweight, const uint16_t* scales,
+                                  const uint32_t* zeros, int group_size, int K, int N,
+                                  void* packed_out);
+
+/* Exact inverse of quick_pack_weights (host). Same array shapes as above, written completely. */
+quick_status_t quick_unpack_weights(const void* packed, int group_size, int K, int N,
+                                    uint32_t* qweight, uint16_t* scales, uint32_t* zeros);
+
+/* The hot path (device, asynchronous on `stream`; no allocation, no host sync, CUDA-graph
+ * capturable).  Y = X . dequant(Wq) with fp32 accumulation (reading R4) and fp16 output.
+ *   X       device, __half [M][K] row-major, 16-byte aligned
+ *   packed  device copy of the quick_pack_weights blob, 128-byte aligned
+ *   Y       device, __half [M][N] row-major, 16-byte aligned
+ * M == 0 is a no-op returning QUICK_OK.  The (K, N, G) given must match the blob. */
+quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N, int K,
+                                int group_size, void* Y, void* stream);
+
+/* Extended form used by tensor parallelism and the tests.
+ *   ldy       row stride of Y in elements (>= N); lets a rank write its column slice in place
+ *   out_fp32  0: Y is __half, 1: Y is float (un-rounded fp32 partial sums for the row-parallel
+ *             fp32 all-reduce)
+ *   tile_n    tokens per MMA tile (16, 32, 64, 128, 256), 0 = automatic
+ *   split_k   CTAs per cluster splitting K (1..8), 0 = automatic
+ * Deterministic: equal inputs and equal (tile_n, split_k) give bit-equal Y. */
+quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K,
+                                   int group_size, void* Y, int ldy, int out_fp32, int tile_n,
+                                   int split_k, void* stream);
+
+/* The launch plan the automatic dispatch would use for (M, N, K, G): tokens per tile,
+ * split-K factor and number of CTAs.  Any out pointer may be NULL. */
+quick_status_t quick_gemm_plan(int M, int N, int K, int group_size, int* tile_n, int* split_k,
+                               int* num_ctas);
+
+/* Device dequantization of a packed blob into W fp16 [K][N] row-major (device), computing
+ * dequant(q)[k][n] bit-exactly as fp16_rne((q - z) * s) (§2.3).  Asynchronous. */
+quick_status_t quick_dequant_weights(const void* packed, int K, int N, int group_size, void* W,
+                                     void* stream);
+
+/* Row-parallel epilogue: dst[i] = fp16_rne(src[i]) for i < n (device float -> device __half). */
+quick_status_t quick_f32_to_f16(const void* src, void* dst, size_t n, void* stream);
+
+/* Column-parallel epilogue: src __half [P][M][Nr] (an all-gather of per-rank Y slices) ->
+ * dst __half [M][P*Nr] row-major (device, asynchronous). */
+quick_status_t quick_gather_columns(const void* src, void* dst, int P, int M, int Nr,
+                                    void* stream);
+
+const char* quick_status_string(quick_status_t status);
+
+/* cudaError_t of the last QUICK_ERR_CUDA returned on the calling thread (0 if none). */
+int quick_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QUICK_H_ */

@@ -1,0 +1,639 @@
+// QUICK W4A16 GEMM for B200 (sm_100a): Y[M][N] = X[M][K] . dequant(Wq)[K][N].
+//
+// PAPER.md: the mixed-precision GEMM of §2.3 with the QUICK idea of §3
+// (P:L78-86): weights are interleaved offline (quick_pack.cpp) so that each thread's direct
+// load, after dequantization in registers (FasterTransformer LOP3 magic), is already
+// in the MMA operand layout -- no shared-memory write-back of dequantized weights and no
+// ldmatrix (Fig. 2).  On Blackwell the operand a thread owns is one TMEM lane of the
+// tcgen05.mma A operand, so the kernel computes the swapped product
+//     D[n][m] = sum_k W^T[n][k] . X^T[k][m]        (A = dequantized weights in TMEM,
+//                                                   B = X tile in SMEM via TMA, D in TMEM)
+// with the weight rows n on the 128-lane MMA M dimension and the tokens m on the MMA N
+// dimension (16..256), so small batches do not waste the 128-row MMA.
+//
+// CTA = 10 warps, warp-specialised:
+//   warp 0      producer: TMA 2-D load of the X tile [BN tokens][64 k] (SWIZZLE_128B) and
+//               1-D bulk copies of the packed int4 stage (4 KiB) + group metadata into a
+//               STAGES-deep mbarrier ring
+//   warp 1      TMEM allocator + MMA issuer (one thread): 4 x tcgen05.mma.kind::f16 per
+//               64-k stage, fp32 accumulation in TMEM (reading R4), tcgen05.commit -> mbarriers
+//   warps 2..9  dequantizers: one LDS.128 of 32 codes (own row) -> 4 x (LOP3 x4, HSUB2/HFMA2
+//               -> exact (q-z), HMUL2 by s) -> tcgen05.st.32x32b.x16 into the TMEM A ring;
+//               then the epilogue (tcgen05.ld -> fp16/fp32 -> Y), or for split-K the fp32
+//               partial -> SMEM, cluster barrier, fixed-order DSMEM reduction (deterministic).
+// Split-K: the S CTAs of a (S,1,1) cluster share one (n-tile, m-tile) and split K (the
+// "split-k" knob of §5); partial sums stay fp32 (tolerance analysis).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/quick.h"
+#include "quick_ptx.cuh"
+
+namespace quick {
+
+constexpr int kThreads = 320;     // 10 warps
+constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
+constexpr int kStageK = 64;       // k per pipeline stage (4 MMAs of K=16)
+constexpr int kAStages = 4;       // depth of the TMEM A-operand ring
+constexpr int kAColsPerStage = 32;              // 64 fp16 of k = 32 x 32-bit TMEM columns
+constexpr int kDCol = kAStages * kAColsPerStage;  // accumulator columns start here
+constexpr int kWStageBytes = kTileRows * kStageK / 2;  // 4 KiB of int4 codes per stage
+constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-tile, group)
+constexpr int kMetaStageBytes = 2 * kMetaBytes;  // a 64-k stage touches <= 2 groups (G % 32 == 0)
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN <= 16 ? 12 : BN <= 32 ? 10 : BN <= 64 ? 7 : BN <= 128 ? 5 : 4;
+  static constexpr int X_BYTES = BN * kStageK * 2;  // [BN][64] fp16, 128-B rows, SW128
+  static constexpr int X_OFF = 0;
+  static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
+  static constexpr int M_OFF = W_OFF + STAGES * kWStageBytes;
+  static constexpr int BAR_OFF = (M_OFF + STAGES * kMetaStageBytes + 7) & ~7;
+  // barriers: full[STAGES], empty[STAGES], afull[4], aempty[4], dfull
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * kAStages + 1;
+  static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;
+  static constexpr int USED = HOLD_OFF + 16;
+  static constexpr int TMEM_COLS = (kDCol + BN <= 256) ? 256 : 512;
+  // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
+  // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
+  static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
+  static constexpr int MIN_SMEM = (228 * 1024) / (MAX_CTAS_PER_SM + 1) + 1024;
+  static constexpr int SMEM_BYTES = (USED + 1024 > MIN_SMEM ? USED + 1024 : MIN_SMEM);
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  // split-K partial tile [BN][128] fp32 reuses the pipeline buffers once the mainloop is done
+  static_assert(BN * kTileRows * 4 <= BAR_OFF, "split-K partial must fit in the pipeline smem");
+};
+
+// ------------------------------------------------------------------------------------------
+// Dequantization of one 32-bit word of the v1 layout (8 codes, nibble order {0,2,4,6,1,3,5,7}
+// along k) into four fp16x2 registers holding (k0,k1), (k2,k3), (k4,k5), (k6,k7).
+//   lo = (w & 0x000f000f) | 0x6400_6400  -> fp16 (1024 + q)          (FT "magic")
+//   hi = (w & 0x00f000f0) | 0x6400_6400  -> fp16 (1024 + 16 q)
+//   (q - z) = lo - (1024 + z)  and  hi * 1/16 - (64 + z): both exact for every (q, z)
+//   w = (q - z) * s with one round-to-nearest-even: bit-identical to the oracle's
+//   fp16_rne((q - z) * s).  Explicit .rn forbids fma contraction.
+// ------------------------------------------------------------------------------------------
+struct DequantConsts {
+  uint32_t zlo;  // fp16x2 (1024 + z)
+  uint32_t zhi;  // fp16x2 -(64 + z)
+  uint32_t s2;   // fp16x2 (s, s)
+};
+
+__device__ __forceinline__ DequantConsts make_consts(uint32_t sbits, uint32_t z) {
+  DequantConsts c;
+  const uint32_t lo = 0x6400u + z;          // 1024 + z   (ulp 1 in [1024, 2048))
+  const uint32_t hi = 0xD400u + 16u * z;    // -(64 + z)  (ulp 1/16 in [64, 128))
+  c.zlo = lo | (lo << 16);
+  c.zhi = hi | (hi << 16);
+  c.s2 = sbits | (sbits << 16);
+  return c;
+}
+
+__device__ __forceinline__ uint32_t hsub2_rn(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hmul2_rn(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t hfma2_rn(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ void dequant_word(uint32_t w, const DequantConsts& c, uint32_t* out) {
+  constexpr uint32_t kMagic = 0x64006400u;
+  constexpr uint32_t kInv16 = 0x2C002C00u;  // fp16x2 (1/16, 1/16)
+  const uint32_t lo0 = ptx::lop3<0xEA>(w, 0x000F000Fu, kMagic);  // (a & b) | c
+  const uint32_t hi0 = ptx::lop3<0xEA>(w, 0x00F000F0u, kMagic);
+  const uint32_t w8 = w >> 8;
+  const uint32_t lo1 = ptx::lop3<0xEA>(w8, 0x000F000Fu, kMagic);
+  const uint32_t hi1 = ptx::lop3<0xEA>(w8, 0x00F000F0u, kMagic);
+  out[0] = hmul2_rn(hsub2_rn(lo0, c.zlo), c.s2);
+  out[1] = hmul2_rn(hfma2_rn(hi0, kInv16, c.zhi), c.s2);
+  out[2] = hmul2_rn(hsub2_rn(lo1, c.zlo), c.s2);
+  out[3] = hmul2_rn(hfma2_rn(hi1, kInv16, c.zhi), c.s2);
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), version 1
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;              // LBO (unused for swizzled K-major), 16 B
+  d |= (uint64_t)(1024u >> 4) << 32;    // SBO = 1024 B between 8-row groups
+  d |= (uint64_t)1u << 46;              // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;              // layout: SWIZZLE_128B
+  return d;
+}
+
+// tcgen05 instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M=128, N=BN
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t instr_desc() {
+  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
+    quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                          const uint8_t* __restrict__ packed, void* __restrict__ Y, int M, int N,
+                          int K, int G, int ldy, int out_fp32) {
+  using C = Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int S = gridDim.x;            // split-K factor (= cluster size)
+  const int split = blockIdx.x;
+  const int t = blockIdx.y;           // n-tile
+  const int m0 = blockIdx.z * BN;     // first token of this tile
+  const int KT = K / kStageK;
+  const int kb = (int)(((long long)split * KT) / S);
+  const int ke = (int)(((long long)(split + 1) * KT) / S);
+  const int nst = ke - kb;
+  const int C32 = K / 32;
+  const int NG = K / G;
+
+  const uint32_t bar_full = sbase + C::BAR_OFF;
+  const uint32_t bar_empty = bar_full + 8 * STAGES;
+  const uint32_t bar_afull = bar_empty + 8 * STAGES;
+  const uint32_t bar_aempty = bar_afull + 8 * kAStages;
+  const uint32_t bar_dfull = bar_aempty + 8 * kAStages;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::HOLD_OFF);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(bar_full + 8 * s, 1);
+      ptx::mbar_init(bar_empty + 8 * s, 8 + 1);  // 8 dequant warps + 1 MMA commit
+    }
+    for (int a = 0; a < kAStages; ++a) {
+      ptx::mbar_init(bar_afull + 8 * a, 8);
+      ptx::mbar_init(bar_aempty + 8 * a, 1);
+    }
+    ptx::mbar_init(bar_dfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
+  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), C::TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
+      const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
+      const uint8_t* wbase = packed + (size_t)t * C32 * kTileRows * 16;
+      const uint8_t* mbase = packed + (size_t)K * N / 2 + (size_t)t * NG * kMetaBytes;
+      for (int it = 0; it < nst; ++it) {
+        const int slot = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
+        const int k0 = (kb + it) * kStageK;
+        const int g0 = k0 / G;
+        const int g1 = (k0 + kStageK - 1) / G;
+        const uint32_t meta_bytes = (uint32_t)(g1 - g0 + 1) * kMetaBytes;
+        const uint32_t full = bar_full + 8 * slot;
+        ptx::mbar_arrive_expect_tx(full, C::X_BYTES + kWStageBytes + meta_bytes);
+        ptx::tma_load_2d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, k0, m0, full, pol_x);
+        ptx::bulk_load_hint(sbase + C::W_OFF + slot * kWStageBytes,
+                            wbase + (size_t)(k0 / 32) * kTileRows * 16, kWStageBytes, full, pol_w);
+        ptx::bulk_load_hint(sbase + C::M_OFF + slot * kMetaStageBytes,
+                            mbase + (size_t)g0 * kMetaBytes, meta_bytes, full, pol_w);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc<BN>();
+      for (int it = 0; it < nst; ++it) {
+        const int slot = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        const int as = it & (kAStages - 1);
+        const uint32_t aph = (uint32_t)(it / kAStages) & 1u;
+        ptx::mbar_wait(bar_full + 8 * slot, ph);     // X tile landed
+        ptx::mbar_wait(bar_afull + 8 * as, aph);     // A stage written by all 8 dequant warps
+        ptx::tc_fence_after();
+        const uint32_t xaddr = sbase + C::X_OFF + slot * C::X_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < kStageK / 16; ++kk) {
+          ptx::mma_f16_ts(tmem + kDCol, tmem + as * kAColsPerStage + kk * 8,
+                          sw128_desc(xaddr + kk * 32), idesc, (it | kk) != 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(bar_empty + 8 * slot);   // X slot free once these MMAs complete
+        ptx::mma_commit(bar_aempty + 8 * as);    // A stage free
+      }
+      ptx::mma_commit(bar_dfull);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ dequantizers
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int h = (warp - 2) >> 2;       // which 32-k chunk of the 64-k stage
+    const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
+    const uint32_t tlane = (uint32_t)(q * 32) << 16;
+    for (int it = 0; it < nst; ++it) {
+      const int slot = it % STAGES;
+      const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+      const int as = it & (kAStages - 1);
+      const uint32_t aph = (uint32_t)(it / kAStages) & 1u;
+      ptx::mbar_wait(bar_full + 8 * slot, ph);
+      const int k0 = (kb + it) * kStageK;
+      const int gi = (k0 + 32 * h) / G - k0 / G;
+      const uint8_t* meta = smem + C::M_OFF + slot * kMetaStageBytes + gi * kMetaBytes;
+      const uint32_t sbits = reinterpret_cast<const uint16_t*>(meta)[r];
+      const uint32_t zbyte = meta[256 + (r >> 1)];
+      const uint4 wv = *reinterpret_cast<const uint4*>(smem + C::W_OFF + slot * kWStageBytes +
+                                                        h * (kWStageBytes / 2) + r * 16);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar_empty + 8 * slot);
+      const DequantConsts dc = make_consts(sbits, (zbyte >> ((r & 1) * 4)) & 0xFu);
+      uint32_t a[16];
+      dequant_word(wv.x, dc, a + 0);
+      dequant_word(wv.y, dc, a + 4);
+      dequant_word(wv.z, dc, a + 8);
+      dequant_word(wv.w, dc, a + 12);
+      ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+      ptx::tc_fence_after();
+      ptx::tmem_st_32x32b_x16(tmem + tlane + as * kAColsPerStage + h * 16, a);
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
+    }
+    // ------------------------------------------------------------------ epilogue part 1
+    constexpr int kColsPerWarp = BN / 2;
+    const int j0 = h * kColsPerWarp;
+    const int n = t * kTileRows + r;
+    if (nst > 0) {
+      ptx::mbar_wait(bar_dfull, 0);
+      ptx::tc_fence_after();
+    }
+    float* part = reinterpret_cast<float*>(smem);  // [BN][128] fp32 (split-K only)
+#pragma unroll 1
+    for (int jc = 0; jc < kColsPerWarp; jc += 8) {
+      uint32_t v[8];
+      if (nst > 0) {
+        ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + j0 + jc, v);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = 0u;
+      }
+      if (S == 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int m = m0 + j0 + jc + i;
+          if (m < M) {
+            const float f = __uint_as_float(v[i]);
+            if (out_fp32)
+              reinterpret_cast<float*>(Y)[(size_t)m * ldy + n] = f;
+            else
+              reinterpret_cast<__half*>(Y)[(size_t)m * ldy + n] = __float2half_rn(f);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) part[(j0 + jc + i) * kTileRows + r] = __uint_as_float(v[i]);
+      }
+    }
+  }
+
+  if (S > 1) {
+    // ---------------------------------------------------------------- split-K reduction
+    // fixed order p = 0..S-1 over the cluster's fp32 partials: deterministic (reading R12)
+    ptx::cluster_sync();
+    const uint32_t my = ptx::cluster_ctarank();
+    constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
+    const int eb = (int)(((int)my * E4) / S) * 4;
+    const int ee = (int)((((int)my + 1) * E4) / S) * 4;
+    for (int e = eb + (int)threadIdx.x * 4; e < ee; e += kThreads * 4) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t local = sbase + (uint32_t)e * 4u;
+      for (int p = 0; p < S; ++p) {
+        const float4 v = ptx::ld_dsmem_f32x4(ptx::mapa(local, (uint32_t)p));
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const int j = e / kTileRows;
+      const int rr = e % kTileRows;
+      const int m = m0 + j;
+      if (m < M) {
+        const size_t o = (size_t)m * ldy + (size_t)t * kTileRows + rr;
+        if (out_fp32) {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + o) = acc;
+        } else {
+          __half2 lo = __floats2half2_rn(acc.x, acc.y);
+          __half2 hi = __floats2half2_rn(acc.z, acc.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(Y) + o) = pk;
+        }
+      }
+    }
+    ptx::cluster_sync();   // peers may still be reading our partials
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Utility kernels on the same layout.
+// ------------------------------------------------------------------------------------------
+// One thread per 16-byte chunk (t, c, r): 32 codes of column n = 128t + r, k = 32c..32c+31.
+__global__ void quick_dequant_kernel(const uint8_t* __restrict__ packed, __half* __restrict__ W,
+                                     int K, int N, int G) {
+  const int C32 = K / 32;
+  const long long total = (long long)(N / kTileRows) * C32 * kTileRows;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int r = (int)(idx % kTileRows);
+  const int c = (int)((idx / kTileRows) % C32);
+  const int t = (int)(idx / ((long long)kTileRows * C32));
+  const uint4 wv = *reinterpret_cast<const uint4*>(packed + idx * 16);
+  const int g = (32 * c) / G;
+  const uint8_t* meta = packed + (size_t)K * N / 2 + ((size_t)t * (K / G) + g) * kMetaBytes;
+  const uint32_t sbits = reinterpret_cast<const uint16_t*>(meta)[r];
+  const uint32_t z = (meta[256 + (r >> 1)] >> ((r & 1) * 4)) & 0xFu;
+  const DequantConsts dc = make_consts(sbits, z);
+  uint32_t a[16];
+  dequant_word(wv.x, dc, a + 0);
+  dequant_word(wv.y, dc, a + 4);
+  dequant_word(wv.z, dc, a + 8);
+  dequant_word(wv.w, dc, a + 12);
+  const int n = t * kTileRows + r;
+  uint16_t* Wb = reinterpret_cast<uint16_t*>(W);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const size_t k = (size_t)32 * c + 2 * i;
+    Wb[k * N + n] = (uint16_t)(a[i] & 0xFFFFu);
+    Wb[(k + 1) * N + n] = (uint16_t)(a[i] >> 16);
+  }
+}
+
+__global__ void quick_f32_to_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst,
+                                        size_t n) {
+  size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x * 4;
+  for (; i + 3 < n; i += stride) {
+    const float4 v = *reinterpret_cast<const float4*>(src + i);
+    *reinterpret_cast<__half2*>(dst + i) = __floats2half2_rn(v.x, v.y);
+    *reinterpret_cast<__half2*>(dst + i + 2) = __floats2half2_rn(v.z, v.w);
+  }
+  for (; i < n; ++i) dst[i] = __float2half_rn(src[i]);
+}
+
+// src [P][M][Nr] -> dst [M][P*Nr], 8 halves (16 B) per thread (Nr % 8 == 0)
+__global__ void quick_gather_columns_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                            int P, int M, int Nr8) {
+  const long long total = (long long)P * M * Nr8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % Nr8);
+    const int m = (int)((i / Nr8) % M);
+    const int p = (int)(i / ((long long)Nr8 * M));
+    dst[((long long)m * P + p) * Nr8 + c] = src[i];
+  }
+}
+
+}  // namespace quick
+
+// ============================================================================================
+// Host side: validation, launch plan, tensor map, launch.
+// ============================================================================================
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+quick_status_t cuda_fail(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return QUICK_ERR_CUDA;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int sm_count() {
+  static int counts[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (counts[dev] == 0) {
+    int c = 0;
+    if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0)
+      c = 148;
+    counts[dev] = c;
+  }
+  return counts[dev];
+}
+
+quick_status_t check_gemm_shape(int M, int N, int K, int G) {
+  if (M < 0 || N <= 0 || K <= 0 || G <= 0) return QUICK_ERR_INVALID_ARG;
+  if (K % G != 0 || N % 8 != 0) return QUICK_ERR_INVALID_ARG;
+  if (N % 128 != 0 || K % 64 != 0 || G % 32 != 0) return QUICK_ERR_UNSUPPORTED;
+  return QUICK_OK;
+}
+
+int auto_tile_n(int M) {
+  if (M <= 16) return 16;
+  if (M <= 32) return 32;
+  if (M <= 64) return 64;
+  if (M <= 128) return 128;
+  return 256;
+}
+
+int ctas_per_sm(int tile_n) { return (quick::kDCol + tile_n <= 256) ? 2 : 1; }
+
+int auto_split(int M, int N, int K, int tile_n) {
+  const int tiles = (N / quick::kTileRows) * ((M + tile_n - 1) / tile_n);
+  const int KT = K / quick::kStageK;
+  const int cap = sm_count() * ctas_per_sm(tile_n);
+  int s = 1;
+  while (s < 8 && tiles * (s + 1) <= cap && KT / (s + 1) >= 4) ++s;
+  return s;
+}
+
+template <int BN>
+quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, int M, int N, int K,
+                         int G, int ldy, int out_fp32, int S, cudaStream_t stream) {
+  using C = quick::Cfg<BN>;
+  auto kern = quick::quick_w4a16_tc_kernel<BN>;
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e);
+    configured[dev] = 1;
+  }
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)S, (unsigned)(N / quick::kTileRows), (unsigned)((M + BN - 1) / BN));
+  cfg.blockDim = dim3(quick::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  cfg.numAttrs = 0;
+  if (S > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  const uint8_t* pk = static_cast<const uint8_t*>(packed);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, pk, Y, M, N, K, G, ldy, out_fp32);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return QUICK_OK;
+}
+
+inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int quick_last_cuda_error(void) { return g_last_cuda_error; }
+
+quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* split_k,
+                               int* num_ctas) {
+  quick_status_t st = check_gemm_shape(M, N, K, G);
+  if (st != QUICK_OK) return st;
+  const int tn = auto_tile_n(M);
+  const int s = auto_split(M, N, K, tn);
+  if (tile_n) *tile_n = tn;
+  if (split_k) *split_k = s;
+  if (num_ctas) *num_ctas = s * (N / quick::kTileRows) * ((M + tn - 1) / tn);
+  return QUICK_OK;
+}
+
+quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K, int G,
+                                   void* Y, int ldy, int out_fp32, int tile_n, int split_k,
+                                   void* stream) {
+  quick_status_t st = check_gemm_shape(M, N, K, G);
+  if (st != QUICK_OK) return st;
+  if (M == 0) return QUICK_OK;
+  if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
+  if (ldy < N) return QUICK_ERR_INVALID_ARG;
+  if (ldy % 8 != 0) return QUICK_ERR_UNSUPPORTED;
+  if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
+  const int tn = tile_n > 0 ? tile_n : auto_tile_n(M);
+  if (tn != 16 && tn != 32 && tn != 64 && tn != 128 && tn != 256) return QUICK_ERR_UNSUPPORTED;
+  const int KT = K / quick::kStageK;
+  int s = split_k > 0 ? split_k : auto_split(M, N, K, tn);
+  if (s < 1 || s > 8 || s > KT)
+    return QUICK_ERR_UNSUPPORTED;
+
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return cuda_fail(cudaErrorInitializationError);
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)quick::kStageK, (cuuint32_t)tn};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(X), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
+
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  switch (tn) {
+    case 16: return launch_bn<16>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
+    case 32: return launch_bn<32>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
+    case 64: return launch_bn<64>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
+    case 128: return launch_bn<128>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
+    default: return launch_bn<256>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
+  }
+}
+
+quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N, int K, int G,
+                                void* Y, void* stream) {
+  return quick_w4a16_gemm_ex(X, packed, M, N, K, G, Y, N, 0, 0, 0, stream);
+}
+
+quick_status_t quick_dequant_weights(const void* packed, int K, int N, int G, void* W,
+                                     void* stream) {
+  quick_status_t st = check_gemm_shape(0, N, K, G);
+  if (st != QUICK_OK) return st;
+  if (!packed || !W) return QUICK_ERR_INVALID_ARG;
+  if (!aligned(packed, 16)) return QUICK_ERR_UNSUPPORTED;
+  const long long total = (long long)(N / 128) * (K / 32) * 128;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((total + threads - 1) / threads);
+  quick::quick_dequant_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(packed), static_cast<__half*>(W), K, N, G);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? QUICK_OK : cuda_fail(e);
+}
+
+quick_status_t quick_f32_to_f16(const void* src, void* dst, size_t n, void* stream) {
+  if (n == 0) return QUICK_OK;
+  if (!src || !dst) return QUICK_ERR_INVALID_ARG;
+  if (!aligned(src, 16) || !aligned(dst, 8)) return QUICK_ERR_UNSUPPORTED;
+  const int threads = 256;
+  unsigned blocks = (unsigned)std::min<size_t>((n / 4 + threads - 1) / threads + 1, 148 * 16);
+  quick::quick_f32_to_f16_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const float*>(src), static_cast<__half*>(dst), n);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? QUICK_OK : cuda_fail(e);
+}
+
+quick_status_t quick_gather_columns(const void* src, void* dst, int P, int M, int Nr,
+                                    void* stream) {
+  if (P <= 0 || M < 0 || Nr <= 0) return QUICK_ERR_INVALID_ARG;
+  if (M == 0) return QUICK_OK;
+  if (!src || !dst) return QUICK_ERR_INVALID_ARG;
+  if (Nr % 8 != 0 || !aligned(src, 16) || !aligned(dst, 16)) return QUICK_ERR_UNSUPPORTED;
+  const long long total = (long long)P * M * (Nr / 8);
+  const int threads = 256;
+  unsigned blocks = (unsigned)std::min<long long>((total + threads - 1) / threads, 148 * 16);
+  quick::quick_gather_columns_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(src), static_cast<uint4*>(dst), P, M, Nr / 8);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? QUICK_OK : cuda_fail(e);
+}
+
+}  // extern "C"

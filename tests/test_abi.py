@@ -1,0 +1,82 @@
+"""The C-ABI library loads, exports every symbol include/quick.h declares, and its host-side
+argument validation returns the documented status codes (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from _helpers import ROOT
+
+quick = pytest.importorskip("paper_2402_10076_b200.quick")
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "quick.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(quick_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for required in ("quick_pack_weights", "quick_w4a16_gemm", "quick_unpack_weights", "quick_packed_bytes"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(quick.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_layout_version_and_sizes():
+    assert quick.quick_layout_version() == 1
+    assert quick.quick_packed_bytes(4096, 4096, 128) == 4096 * 4096 // 2 + 32 * 4096 * 5 // 2
+    assert quick.quick_packed_bytes(8192, 28672, 128) == 8192 * 28672 // 2 + 64 * 28672 * 5 // 2
+    assert quick.quick_packed_bytes(512, 100, 128) == 0     # N % 8
+    assert quick.quick_packed_bytes(100, 128, 4) == 0       # K % 64 / G % 32
+    assert quick.quick_packed_bytes(0, 128, 128) == 0
+
+
+def test_status_strings():
+    for s, name in enumerate(["QUICK_OK", "QUICK_ERR_INVALID_ARG", "QUICK_ERR_UNSUPPORTED", "QUICK_ERR_CUDA"]):
+        assert quick.quick_status_string(s) == name
+
+
+def test_gemm_argument_validation_before_any_cuda_call():
+    lib = quick.raw_library()
+    null = ctypes.c_void_p(0)
+    dummy = ctypes.c_void_p(1 << 20)
+    # M == 0 is a no-op, even with null pointers (BLAS convention, reading R15)
+    assert lib.quick_w4a16_gemm(null, null, 0, 256, 512, 128, null, null) == quick.QUICK_OK
+    assert lib.quick_w4a16_gemm(dummy, dummy, -1, 256, 512, 128, dummy, null) == quick.QUICK_ERR_INVALID_ARG
+    assert lib.quick_w4a16_gemm(dummy, dummy, 8, 256, 500, 128, dummy, null) == quick.QUICK_ERR_INVALID_ARG
+    assert lib.quick_w4a16_gemm(dummy, dummy, 8, 200, 512, 128, dummy, null) == quick.QUICK_ERR_UNSUPPORTED
+    assert lib.quick_w4a16_gemm(dummy, dummy, 8, 256, 512, 16, dummy, null) == quick.QUICK_ERR_UNSUPPORTED
+    assert lib.quick_w4a16_gemm(null, dummy, 8, 256, 512, 128, dummy, null) == quick.QUICK_ERR_INVALID_ARG
+    # misaligned X (16 B required)
+    assert lib.quick_w4a16_gemm(ctypes.c_void_p((1 << 20) + 2), dummy, 8, 256, 512, 128, dummy, null) == \
+        quick.QUICK_ERR_UNSUPPORTED
+    # _ex overrides
+    ex = lib.quick_w4a16_gemm_ex
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 100, 0, 0, 0, null) == quick.QUICK_ERR_INVALID_ARG   # ldy < N
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 260, 0, 0, 0, null) == quick.QUICK_ERR_UNSUPPORTED  # ldy % 8
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 48, 0, null) == quick.QUICK_ERR_UNSUPPORTED  # tile
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 16, 9, null) == quick.QUICK_ERR_UNSUPPORTED  # split>8
+    assert ex(dummy, dummy, 8, 256, 128, 128, dummy, 256, 0, 16, 3, null) == quick.QUICK_ERR_UNSUPPORTED  # split>KT
+
+
+def test_plan_validation():
+    with pytest.raises(quick.QuickError):
+        quick.quick_gemm_plan(8, 200, 512, 128)
+
+
+def test_epilogue_validation():
+    lib = quick.raw_library()
+    null = ctypes.c_void_p(0)
+    assert lib.quick_f32_to_f16(null, null, 0, null) == quick.QUICK_OK
+    assert lib.quick_f32_to_f16(null, null, 8, null) == quick.QUICK_ERR_INVALID_ARG
+    assert lib.quick_gather_columns(null, null, 0, 4, 8, null) == quick.QUICK_ERR_INVALID_ARG
+    d = ctypes.c_void_p(1 << 20)
+    assert lib.quick_gather_columns(d, d, 2, 4, 12, null) == quick.QUICK_ERR_UNSUPPORTED
+    assert lib.quick_dequant_weights(null, 512, 256, 128, null, null) == quick.QUICK_ERR_INVALID_ARG

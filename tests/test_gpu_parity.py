@@ -1,0 +1,204 @@
+"""GPU parity: the sm_100a path through the C-ABI against the CPU oracle (marker: gpu).
+
+Bars: dequantization bit-exact; GEMM within the north-star tolerance
+(rel 1e-2, abs 1e-3 where |ref| < 1e-2); bit-exact where the exact result is representable
+(one-hot X, integer-exact regime, zero weights); run-to-run bit-identical.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no GPU", allow_module_level=True)
+
+from paper_2402_10076_b200 import quick  # noqa: E402  (fails loudly if libquick.so is missing)
+
+DEV = torch.device("cuda:0")
+
+
+def to_dev_f16(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.float16).to(DEV)
+
+
+def pack_dev(p):
+    return torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, p.group_size)).to(DEV)
+
+
+def run(p, **kw):
+    y = quick.quick_w4a16_gemm(to_dev_f16(p.x), pack_dev(p), p.N, p.K, p.group_size, **kw)
+    torch.cuda.synchronize()
+    return y
+
+
+def f16_bits(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+# ------------------------------------------------------------------------------- dequant
+@pytest.mark.parametrize("K,N,G", [(512, 256, 128), (256, 384, 32), (192, 256, 96), (4096, 4096, 128)])
+def test_dequant_bit_exact(K, N, G):
+    p = synth.make_problem(K ^ N, M=1, N=N, K=K, G=G)
+    w = quick.quick_dequant_weights(pack_dev(p), K, N, G)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(f16_bits(w), oracle.dequant(p.qweight, p.scales, p.zeros, G).view(np.uint16))
+
+
+def test_dequant_bit_exact_all_codes_zeros_and_extreme_scales():
+    """Every (q, z) pair against scales incl. subnormal, huge (overflow), negative, +-0."""
+    K, G = 64, 32
+    scale_bits = np.array([0x0001, 0x0003, 0x03FF, 0x0400, 0x2E66, 0x3800, 0x3C00, 0x3C01, 0x5BFF, 0x7BFF,
+                           0x8000, 0x0000, 0xBC00, 0x8001, 0x1C00, 0x2400], dtype=np.uint16)
+    N = 16 * 16 * 2 * 8   # (z, s) per column, padded to 128
+    N = ((N + 127) // 128) * 128
+    cols = np.arange(N)
+    z = (cols % 16).astype(np.uint8)
+    s = scale_bits[(cols // 16) % scale_bits.size]
+    codes = np.tile((np.arange(K) % 16).astype(np.uint8)[:, None], (1, N))
+    qweight = oracle.pack_awq(codes)
+    zeros = oracle.pack_awq(np.tile(z[None, :], (K // G, 1)))
+    scales = np.tile(s[None, :], (K // G, 1)).view(np.float16)
+    blob = torch.from_numpy(quick.quick_pack_weights(qweight, scales, zeros, G)).to(DEV)
+    w = quick.quick_dequant_weights(blob, K, N, G)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(f16_bits(w), oracle.dequant(qweight, scales, zeros, G).view(np.uint16))
+
+
+# ------------------------------------------------------------------------------- GEMM: exact sets
+@pytest.mark.parametrize("tile_n,split_k", [(0, 0), (16, 1), (32, 2), (64, 4), (128, 1), (256, 2)])
+def test_onehot_rows_bit_exact(tile_n, split_k):
+    p = synth.make_structured("onehot", 3, M=16, N=256, K=512, G=128)
+    y = run(p, tile_n=tile_n, split_k=split_k)
+    ref = oracle.round_fp16(oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128))
+    np.testing.assert_array_equal(f16_bits(y), ref.view(np.uint16))
+
+
+@pytest.mark.parametrize("M,tile_n,split_k", [(9, 0, 0), (40, 32, 3), (130, 128, 2), (256, 256, 4), (5, 16, 8)])
+def test_integer_exact_regime_bit_exact(M, tile_n, split_k):
+    p = synth.make_structured("intexact", 5, M=M, N=384, K=1024, G=128)
+    y = run(p, tile_n=tile_n, split_k=split_k)
+    ref = oracle.round_fp16(oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128))
+    np.testing.assert_array_equal(f16_bits(y), ref.view(np.uint16))
+
+
+def test_zero_weights_give_zero():
+    p = synth.make_structured("zero_weights", 4, M=33, N=256, K=512, G=64)
+    y = run(p)
+    assert torch.count_nonzero(y.float()).item() == 0
+
+
+# ------------------------------------------------------------------------------- GEMM: tolerance
+def check_tol(p, y, label=""):
+    ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, p.group_size)
+    res = oracle.tol_check(y.float().cpu().numpy(), ref)
+    assert res["ok"], (label, res)
+    return res
+
+
+def test_tiny_config_all_paths():
+    """BASELINE.json configs[0]: M=8, N=256, K=512, G=128."""
+    p = synth.make_problem(0, M=8, N=256, K=512, G=128)
+    for tile_n in (0, 16, 32, 64, 128, 256):
+        for split_k in (0, 1, 2, 4, 8):
+            check_tol(p, run(p, tile_n=tile_n, split_k=split_k), (tile_n, split_k))
+
+
+@pytest.mark.parametrize("M", [1, 3, 15, 16, 17, 31, 33, 64, 100, 128, 129, 255, 256, 257, 300])
+def test_tails_and_tiles(M):
+    p = synth.make_problem(M, M=M, N=512, K=1024, G=128)
+    check_tol(p, run(p), M)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_unit_scale_stress(seed):
+    p = synth.make_structured("unit", seed, M=24, N=256, K=2048, G=128)
+    check_tol(p, run(p))
+
+
+@pytest.mark.parametrize("G", [32, 64, 96, 256])
+def test_group_sizes(G):
+    p = synth.make_problem(G, M=20, N=256, K=768 if G == 256 else 1536, G=G)
+    if p.K % G:
+        pytest.skip("K not a multiple of G")
+    check_tol(p, run(p))
+    check_tol(p, run(p, split_k=3))
+
+
+@pytest.mark.parametrize("M", [1, 2, 4, 8, 16, 32, 64, 128, 256])
+def test_llama7b_attention_sweep(M):
+    """BASELINE.json configs[1]: N = K = 4096, g128, full-output parity."""
+    p = synth.make_problem(100 + M, M=M, N=4096, K=4096, G=128)
+    check_tol(p, run(p), M)
+
+
+def test_fp32_output_and_ldy():
+    p = synth.make_problem(6, M=40, N=256, K=512, G=128)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+    y32 = quick.quick_w4a16_gemm(x, blob, 256, 512, 128, out_fp32=True)
+    big = torch.full((40, 512), 7.0, device=DEV, dtype=torch.float16)
+    quick.quick_w4a16_gemm(x, blob, 256, 512, 128, out=big[:, 128:384], ldy=512)
+    torch.cuda.synchronize()
+    assert oracle.tol_check(y32.cpu().numpy(), ref)["ok"]
+    assert np.max(np.abs(y32.cpu().numpy() - ref)) < 1e-4
+    assert oracle.tol_check(big[:, 128:384].float().cpu().numpy(), ref)["ok"]
+    assert torch.all(big[:, :128] == 7.0) and torch.all(big[:, 384:] == 7.0)
+
+
+def test_deterministic_run_to_run():
+    p = synth.make_problem(12, M=16, N=1024, K=4096, G=128)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    ys = [quick.quick_w4a16_gemm(x, blob, 1024, 4096, 128, split_k=8) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(ys[0].view(torch.int16), y.view(torch.int16)) for y in ys[1:])
+
+
+def test_raw_c_abi_entry_point():
+    p = synth.make_problem(13, M=5, N=256, K=512, G=128)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    y = torch.empty((5, 256), device=DEV, dtype=torch.float16)
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), 5, 256, 512, 128, y.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    check_tol(p, y)
+
+
+def test_epilogue_kernels():
+    src = torch.randn(1000, device=DEV, dtype=torch.float32) * 100
+    dst = quick.quick_f32_to_f16(src)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(f16_bits(dst), src.cpu().numpy().astype(np.float16).view(np.uint16))
+    P, M, Nr = 4, 3, 256
+    g = torch.randn(P, M, Nr, device=DEV).half()
+    out = quick.quick_gather_columns(g, P, M, Nr)
+    torch.cuda.synchronize()
+    expect = np.concatenate([g[p].cpu().numpy() for p in range(P)], axis=1)
+    np.testing.assert_array_equal(out.cpu().numpy(), expect)
+
+
+# ------------------------------------------------------------------------------- full-size configs
+def _sampled_cols_check(p, y, cols):
+    """Oracle on sampled output columns only (dequantize just those columns)."""
+    G = p.group_size
+    q = oracle.unpack_awq(p.qweight)[:, cols]
+    z = oracle.unpack_awq(p.zeros)[:, cols]
+    s = p.scales[:, cols]
+    w = oracle.dequant(oracle.pack_awq(q), s, oracle.pack_awq(z), G)
+    ref = oracle.gemm(p.x, w)
+    res = oracle.tol_check(y.float().cpu().numpy()[:, cols], ref)
+    assert res["ok"], res
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 13824, 5120), (512, 5120, 13824), (64, 28672, 8192),
+                                   (1024, 28672, 8192), (256, 8192, 28672)])
+def test_full_size_shapes_sampled(M, N, K):
+    p = synth.make_problem(M + N, M=M, N=N, K=K, G=128)
+    y = run(p)
+    rng = np.random.default_rng(M)
+    cols = np.unique(np.concatenate([np.arange(8), np.arange(N - 8, N), rng.choice(N, 240, replace=False)]))
+    cols = cols[:len(cols) // 8 * 8]
+    _sampled_cols_check(p, y, cols)
