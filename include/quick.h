@@ -68,15 +68,23 @@ quick_status_t quick_unpack_weights(const void* packed, int group_size, int K, i
 quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N, int K,
                                 int group_size, void* Y, void* stream);
 
-/* Extended form used by tensor parallelism and the tests.
- *   ldy       row stride of Y in elements (>= N); lets a rank write its column slice in place
- *   out_fp32  0: Y is __half, 1: Y is float (un-rounded fp32 partial sums for the row-parallel
- *             fp32 all-reduce)
+/* Flags of quick_w4a16_gemm_ex. */
+#define QUICK_FLAG_OUT_F32 1 /* Y is float: un-rounded fp32 sums (row-parallel fp32 all-reduce) */
+#define QUICK_FLAG_PDL 2     /* launch with programmatic dependent launch: the kernel's prologue
+                                and its (read-only) weight stream may overlap the previous
+                                kernel in the stream; X is read and Y written only after that
+                                kernel completes.  The weights must not be written by the
+                                immediately preceding kernel. */
+
+/* Extended form used by tensor parallelism, layer stacks and the tests.
+ *   ldy       row stride of Y in elements (>= N, multiple of 8); lets a rank write its column
+ *             slice of a wider Y in place
+ *   flags     QUICK_FLAG_* bits (0 = fp16 Y, ordinary stream ordering)
  *   tile_n    tokens per MMA tile (16, 32, 64, 128, 256), 0 = automatic
- *   split_k   CTAs per cluster splitting K (1..8), 0 = automatic
+ *   split_k   CTAs per cluster splitting K (1..8, <= K/64), 0 = automatic
  * Deterministic: equal inputs and equal (tile_n, split_k) give bit-equal Y. */
 quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K,
-                                   int group_size, void* Y, int ldy, int out_fp32, int tile_n,
+                                   int group_size, void* Y, int ldy, int flags, int tile_n,
                                    int split_k, void* stream);
 
 /* The launch plan the automatic dispatch would use for (M, N, K, G): tokens per tile,

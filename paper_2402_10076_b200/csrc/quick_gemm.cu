@@ -46,6 +46,7 @@ constexpr int kDCol = kAStages * kAColsPerStage;  // accumulator columns start h
 constexpr int kWStageBytes = kTileRows * kStageK / 2;  // 4 KiB of int4 codes per stage
 constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-tile, group)
 constexpr int kMetaStageBytes = 2 * kMetaBytes;  // a 64-k stage touches <= 2 groups (G % 32 == 0)
+constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable clusters)
 
 template <int BN>
 struct Cfg {
@@ -147,7 +148,7 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const uint8_t* __restrict__ packed, void* __restrict__ Y, int M, int N,
-                          int K, int G, int ldy, int out_fp32) {
+                          int K, int G, int g_shift, int ldy, int flags) {
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -193,6 +194,14 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  // let the next kernel in the stream launch its prologue early (PDL); it still waits for
+  // this grid's completion before touching anything this grid writes
+  ptx::griddep_launch_dependents();
+
+  const bool out_fp32 = (flags & QUICK_FLAG_OUT_F32) != 0;
+  const bool pdl = (flags & QUICK_FLAG_PDL) != 0;
+  // group index of k: shift when G is a power of two, division otherwise
+  auto group_of = [&](int k) { return g_shift >= 0 ? (k >> g_shift) : (k / G); };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
@@ -201,21 +210,37 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
       const uint8_t* wbase = packed + (size_t)t * C32 * kTileRows * 16;
       const uint8_t* mbase = packed + (size_t)K * N / 2 + (size_t)t * NG * kMetaBytes;
+      // Weights and metadata are read-only for this call: their bulk copies may be issued
+      // before the programmatic grid dependency resolves; X may be produced by the previous
+      // kernel, so its TMA waits for it (PDL).
+      const int pre = pdl ? (nst < STAGES ? nst : STAGES) : 0;
+      int slot = 0;
+      uint32_t ph = 0;
       for (int it = 0; it < nst; ++it) {
-        const int slot = it % STAGES;
-        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-        ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
+        if (it >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
         const int k0 = (kb + it) * kStageK;
-        const int g0 = k0 / G;
-        const int g1 = (k0 + kStageK - 1) / G;
+        const int g0 = group_of(k0);
+        const int g1 = group_of(k0 + kStageK - 1);
         const uint32_t meta_bytes = (uint32_t)(g1 - g0 + 1) * kMetaBytes;
         const uint32_t full = bar_full + 8 * slot;
         ptx::mbar_arrive_expect_tx(full, C::X_BYTES + kWStageBytes + meta_bytes);
-        ptx::tma_load_2d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, k0, m0, full, pol_x);
         ptx::bulk_load_hint(sbase + C::W_OFF + slot * kWStageBytes,
                             wbase + (size_t)(k0 / 32) * kTileRows * 16, kWStageBytes, full, pol_w);
         ptx::bulk_load_hint(sbase + C::M_OFF + slot * kMetaStageBytes,
                             mbase + (size_t)g0 * kMetaBytes, meta_bytes, full, pol_w);
+        if (it == pre - 1 || (pre == 0 && it == 0)) {
+          if (pdl) ptx::griddep_wait();
+          // X loads of the stages issued so far (weights went first)
+          int s2 = 0;
+          for (int j = 0; j <= it; ++j) {
+            ptx::tma_load_2d_hint(sbase + C::X_OFF + s2 * C::X_BYTES, &tmap_x, (kb + j) * kStageK, m0,
+                                  bar_full + 8 * s2, pol_x);
+            s2 = (s2 + 1 == STAGES) ? 0 : s2 + 1;
+          }
+        } else if (it >= pre) {
+          ptx::tma_load_2d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, k0, m0, full, pol_x);
+        }
+        if (++slot == STAGES) { slot = 0; ph ^= 1u; }
       }
     }
     __syncwarp();
@@ -223,11 +248,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     // ------------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc<BN>();
+      int slot = 0, as = 0;
+      uint32_t ph = 0, aph = 0;
       for (int it = 0; it < nst; ++it) {
-        const int slot = it % STAGES;
-        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-        const int as = it & (kAStages - 1);
-        const uint32_t aph = (uint32_t)(it / kAStages) & 1u;
         ptx::mbar_wait(bar_full + 8 * slot, ph);     // X tile landed
         ptx::mbar_wait(bar_afull + 8 * as, aph);     // A stage written by all 8 dequant warps
         ptx::tc_fence_after();
@@ -239,6 +262,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         }
         ptx::mma_commit(bar_empty + 8 * slot);   // X slot free once these MMAs complete
         ptx::mma_commit(bar_aempty + 8 * as);    // A stage free
+        if (++slot == STAGES) { slot = 0; ph ^= 1u; }
+        if (++as == kAStages) { as = 0; aph ^= 1u; }
       }
       ptx::mma_commit(bar_dfull);
     }
@@ -249,14 +274,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     const int h = (warp - 2) >> 2;       // which 32-k chunk of the 64-k stage
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
+    int slot = 0, as = 0;
+    uint32_t ph = 0, aph = 0;
     for (int it = 0; it < nst; ++it) {
-      const int slot = it % STAGES;
-      const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-      const int as = it & (kAStages - 1);
-      const uint32_t aph = (uint32_t)(it / kAStages) & 1u;
       ptx::mbar_wait(bar_full + 8 * slot, ph);
       const int k0 = (kb + it) * kStageK;
-      const int gi = (k0 + 32 * h) / G - k0 / G;
+      const int gi = group_of(k0 + 32 * h) - group_of(k0);
       const uint8_t* meta = smem + C::M_OFF + slot * kMetaStageBytes + gi * kMetaBytes;
       const uint32_t sbits = reinterpret_cast<const uint16_t*>(meta)[r];
       const uint32_t zbyte = meta[256 + (r >> 1)];
@@ -277,6 +300,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
+      if (++slot == STAGES) { slot = 0; ph ^= 1u; }
+      if (++as == kAStages) { as = 0; aph ^= 1u; }
     }
     // ------------------------------------------------------------------ epilogue part 1
     constexpr int kColsPerWarp = BN / 2;
@@ -318,22 +343,30 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
 
   if (S > 1) {
     // ---------------------------------------------------------------- split-K reduction
-    // fixed order p = 0..S-1 over the cluster's fp32 partials: deterministic (reading R12)
+    // fixed order p = 0..S-1 over the cluster's fp32 partials: deterministic (reading R12).
+    // All S DSMEM loads of an element are issued before the first add (latency ~200 cycles).
     ptx::cluster_sync();
     const uint32_t my = ptx::cluster_ctarank();
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
     const int eb = (int)(((int)my * E4) / S) * 4;
     const int ee = (int)((((int)my + 1) * E4) / S) * 4;
+    uint32_t peer[kMaxSplit];
+#pragma unroll
+    for (int p = 0; p < kMaxSplit; ++p) peer[p] = ptx::mapa(sbase, (uint32_t)(p < S ? p : 0));
     for (int e = eb + (int)threadIdx.x * 4; e < ee; e += kThreads * 4) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      const uint32_t local = sbase + (uint32_t)e * 4u;
-      for (int p = 0; p < S; ++p) {
-        const float4 v = ptx::ld_dsmem_f32x4(ptx::mapa(local, (uint32_t)p));
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
-      }
+      float4 v[kMaxSplit];
+#pragma unroll
+      for (int p = 0; p < kMaxSplit; ++p)
+        if (p < S) v[p] = ptx::ld_dsmem_f32x4(peer[p] + (uint32_t)e * 4u);
+      float4 acc = v[0];
+#pragma unroll
+      for (int p = 1; p < kMaxSplit; ++p)
+        if (p < S) {
+          acc.x += v[p].x;
+          acc.y += v[p].y;
+          acc.z += v[p].z;
+          acc.w += v[p].w;
+        }
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
       const int m = m0 + j;
@@ -454,11 +487,24 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-int sm_count() {
-  static int counts[64] = {0};
+constexpr int kMaxDev = 64;
+constexpr int kTiles[5] = {16, 32, 64, 128, 256};
+
+int tile_index(int bn) {
+  for (int i = 0; i < 5; ++i)
+    if (kTiles[i] == bn) return i;
+  return -1;
+}
+
+int current_device() {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (dev < 0 || dev >= 64) return 148;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 0;
+  return dev;
+}
+
+int sm_count() {
+  static int counts[kMaxDev] = {0};
+  const int dev = current_device();
   if (counts[dev] == 0) {
     int c = 0;
     if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0)
@@ -475,57 +521,171 @@ quick_status_t check_gemm_shape(int M, int N, int K, int G) {
   return QUICK_OK;
 }
 
-int auto_tile_n(int M) {
-  if (M <= 16) return 16;
-  if (M <= 32) return 32;
-  if (M <= 64) return 64;
-  if (M <= 128) return 128;
-  return 256;
+template <int BN>
+void* kernel_ptr() {
+  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN>);
+}
+void* kernel_for(int bn) {
+  switch (bn) {
+    case 16: return kernel_ptr<16>();
+    case 32: return kernel_ptr<32>();
+    case 64: return kernel_ptr<64>();
+    case 128: return kernel_ptr<128>();
+    default: return kernel_ptr<256>();
+  }
+}
+int smem_for(int bn) {
+  switch (bn) {
+    case 16: return quick::Cfg<16>::SMEM_BYTES;
+    case 32: return quick::Cfg<32>::SMEM_BYTES;
+    case 64: return quick::Cfg<64>::SMEM_BYTES;
+    case 128: return quick::Cfg<128>::SMEM_BYTES;
+    default: return quick::Cfg<256>::SMEM_BYTES;
+  }
 }
 
-int ctas_per_sm(int tile_n) { return (quick::kDCol + tile_n <= 256) ? 2 : 1; }
+// one-time per (device, tile): opt into the dynamic shared memory the config needs
+cudaError_t configure_kernel(int bn) {
+  static std::mutex mu;
+  static bool done[kMaxDev][5] = {};
+  const int dev = current_device(), ti = tile_index(bn);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done[dev][ti]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_for(bn));
+  if (e == cudaSuccess) done[dev][ti] = true;
+  return e;
+}
 
-int auto_split(int M, int N, int K, int tile_n) {
-  const int tiles = (N / quick::kTileRows) * ((M + tile_n - 1) / tile_n);
+// How many clusters of S CTAs (or, for S == 1, CTAs) can be resident at once on this device.
+// Cluster placement is GPC-constrained, so this is not simply SMs * CTAs-per-SM / S.
+int max_resident(int bn, int S) {
+  static std::mutex mu;
+  static int cache[kMaxDev][5][quick::kMaxSplit + 1] = {};
+  const int dev = current_device(), ti = tile_index(bn);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache[dev][ti][S]) return cache[dev][ti][S];
+  }
+  int n = 0;
+  if (configure_kernel(bn) == cudaSuccess) {
+    if (S == 1) {
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(bn), quick::kThreads,
+                                                        smem_for(bn)) == cudaSuccess)
+        n = per_sm * sm_count();
+    } else {
+      cudaLaunchConfig_t cfg;
+      std::memset(&cfg, 0, sizeof(cfg));
+      cfg.gridDim = dim3((unsigned)S, 1, 1);
+      cfg.blockDim = dim3(quick::kThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem_for(bn);
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = (unsigned)S;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, kernel_for(bn), &cfg) != cudaSuccess) n = 0;
+    }
+  }
+  cudaGetLastError();  // occupancy queries must not leave a sticky error behind
+  if (n <= 0) n = (S == 1 ? sm_count() : sm_count() / (2 * S));
+  if (n <= 0) n = 1;
+  std::lock_guard<std::mutex> lock(mu);
+  cache[dev][ti][S] = n;
+  return n;
+}
+
+struct Plan {
+  int tile_n, split, ctas;
+  double cost;
+};
+
+// Cost model in SM cycles.  Per 64-k stage a CTA needs max(MMA, dequant)
+// cycles: MMA 4 x (BN / 2) (4096 fp16 MAC/clk/SM), dequant ~kDequantCycles for 8192 weights;
+// a wave of CTAs pays a fixed prologue/epilogue; split-K adds a DSMEM reduction; the chip
+// cannot beat HBM for the weights nor L2 for the X re-reads.
+constexpr double kDequantCycles = 110.0;
+constexpr double kFixedCycles = 2500.0;
+constexpr double kHbmBytesPerCycle = 3300.0;   // ~6.5 TB/s at ~1.9 GHz
+constexpr double kL2BytesPerCycle = 5500.0;
+constexpr double kDsmemBytesPerCycle = 18.0;
+
+Plan evaluate(int M, int N, int K, int G, int bn, int S) {
   const int KT = K / quick::kStageK;
-  const int cap = sm_count() * ctas_per_sm(tile_n);
-  int s = 1;
-  while (s < 8 && tiles * (s + 1) <= cap && KT / (s + 1) >= 4) ++s;
-  return s;
+  const int n_tiles = N / quick::kTileRows;
+  const int m_tiles = (M + bn - 1) / bn;
+  const int tiles = n_tiles * m_tiles;
+  const int resident = max_resident(bn, S);
+  const int waves = (tiles + resident - 1) / resident;
+  const int stages = (KT + S - 1) / S;
+  const double per_stage = std::max(2.0 * bn, kDequantCycles);
+  double t_cta = stages * per_stage + kFixedCycles;
+  if (S > 1) t_cta += 800.0 + (double)bn * quick::kTileRows * 4.0 * (S - 1) / S / kDsmemBytesPerCycle;
+  const double wbytes = (double)K * N / 2 + (double)(K / G) * N * 2.5;
+  const double xbytes = (double)n_tiles * M * K * 2;
+  const double cost = std::max({waves * t_cta, wbytes * m_tiles / kHbmBytesPerCycle + kFixedCycles,
+                                xbytes / kL2BytesPerCycle + kFixedCycles});
+  return Plan{bn, S, tiles * S, cost};
+}
+
+Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
+  const int KT = K / quick::kStageK;
+  Plan best{0, 0, 0, 1e300};
+  for (int ti = 0; ti < 5; ++ti) {
+    const int bn = kTiles[ti];
+    if (force_tile > 0 && bn != force_tile) continue;
+    // candidate tiles: the smallest tile covering M, and (for larger M) one or two smaller
+    // tiles, which trade extra dequantization for fewer split-K partials
+    const int cover = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    if (force_tile <= 0 && (bn > cover || bn * 4 < cover)) continue;
+    for (int S = 1; S <= quick::kMaxSplit && S <= KT; ++S) {
+      if (force_split > 0 && S != force_split) continue;
+      Plan p = evaluate(M, N, K, G, bn, S);
+      if (p.cost < best.cost * 0.97) best = p;   // prefer the earlier (smaller S) on near-ties
+    }
+  }
+  return best;
 }
 
 template <int BN>
 quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, int M, int N, int K,
-                         int G, int ldy, int out_fp32, int S, cudaStream_t stream) {
+                         int G, int ldy, int flags, int S, cudaStream_t stream) {
   using C = quick::Cfg<BN>;
-  auto kern = quick::quick_w4a16_tc_kernel<BN>;
-  static int configured[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
-    if (e != cudaSuccess) return cuda_fail(e);
-    configured[dev] = 1;
-  }
+  cudaError_t e = configure_kernel(BN);
+  if (e != cudaSuccess) return cuda_fail(e);
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)S, (unsigned)(N / quick::kTileRows), (unsigned)((M + BN - 1) / BN));
   cfg.blockDim = dim3(quick::kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  cfg.numAttrs = 0;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   if (S > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)S;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)S;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (flags & QUICK_FLAG_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  int g_shift = -1;
+  if ((G & (G - 1)) == 0) {
+    g_shift = 0;
+    while ((1 << g_shift) < G) ++g_shift;
   }
   const uint8_t* pk = static_cast<const uint8_t*>(packed);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmap, pk, Y, M, N, K, G, ldy, out_fp32);
+  e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN>, tmap, pk, Y, M, N, K, G, g_shift,
+                         ldy, flags);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
 }
@@ -542,30 +702,30 @@ quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* spl
                                int* num_ctas) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
-  const int tn = auto_tile_n(M);
-  const int s = auto_split(M, N, K, tn);
-  if (tile_n) *tile_n = tn;
-  if (split_k) *split_k = s;
-  if (num_ctas) *num_ctas = s * (N / quick::kTileRows) * ((M + tn - 1) / tn);
+  const Plan p = choose_plan(M > 0 ? M : 1, N, K, G, 0, 0);
+  if (tile_n) *tile_n = p.tile_n;
+  if (split_k) *split_k = p.split;
+  if (num_ctas) *num_ctas = p.ctas;
   return QUICK_OK;
 }
 
 quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K, int G,
-                                   void* Y, int ldy, int out_fp32, int tile_n, int split_k,
+                                   void* Y, int ldy, int flags, int tile_n, int split_k,
                                    void* stream) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
   if (M == 0) return QUICK_OK;
   if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
-  if (ldy % 8 != 0) return QUICK_ERR_UNSUPPORTED;
-  if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
-  const int tn = tile_n > 0 ? tile_n : auto_tile_n(M);
-  if (tn != 16 && tn != 32 && tn != 64 && tn != 128 && tn != 256) return QUICK_ERR_UNSUPPORTED;
-  const int KT = K / quick::kStageK;
-  int s = split_k > 0 ? split_k : auto_split(M, N, K, tn);
-  if (s < 1 || s > 8 || s > KT)
+  if (ldy % 8 != 0 || (flags & ~(QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL)) != 0)
     return QUICK_ERR_UNSUPPORTED;
+  if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
+  if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
+  const int KT = K / quick::kStageK;
+  if (split_k < 0 || split_k > quick::kMaxSplit || split_k > KT) return QUICK_ERR_UNSUPPORTED;
+
+  const Plan plan = choose_plan(M, N, K, G, tile_n, split_k);
+  const int tn = plan.tile_n, s = plan.split;
 
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return cuda_fail(cudaErrorInitializationError);
@@ -581,11 +741,11 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
 
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
   switch (tn) {
-    case 16: return launch_bn<16>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
-    case 32: return launch_bn<32>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
-    case 64: return launch_bn<64>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
-    case 128: return launch_bn<128>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
-    default: return launch_bn<256>(tmap, packed, Y, M, N, K, G, ldy, out_fp32, s, strm);
+    case 16: return launch_bn<16>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 32: return launch_bn<32>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 64: return launch_bn<64>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 128: return launch_bn<128>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    default: return launch_bn<256>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
   }
 }
 

@@ -13,6 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libquick.so")
 
 QUICK_OK, QUICK_ERR_INVALID_ARG, QUICK_ERR_UNSUPPORTED, QUICK_ERR_CUDA = 0, 1, 2, 3
+QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL = 1, 2
 
 
 class QuickError(RuntimeError):
@@ -115,7 +116,7 @@ def quick_gemm_plan(M: int, N: int, K: int, group_size: int):
 
 # ----------------------------------------------------------------------------- device side
 def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ldy=None, out_fp32=False,
-                     tile_n: int = 0, split_k: int = 0, stream=None):
+                     pdl=False, tile_n: int = 0, split_k: int = 0, stream=None):
     """Y = X . dequant(Wq) on the GPU.  x: cuda fp16 [M][K]; packed: cuda uint8 blob.
     Returns `out` (allocated if None): fp16 [M][N] (fp32 if out_fp32)."""
     import torch
@@ -127,13 +128,19 @@ def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ld
     ld = out.stride(0) if ldy is None else ldy
     _check("quick_w4a16_gemm_ex", _lib.quick_w4a16_gemm_ex(
         ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(packed.data_ptr()), M, N, K, group_size,
-        ctypes.c_void_p(out.data_ptr()), ld, 1 if out_fp32 else 0, tile_n, split_k, _stream_handle(stream)))
+        ctypes.c_void_p(out.data_ptr()), ld, (QUICK_FLAG_OUT_F32 if out_fp32 else 0) | (QUICK_FLAG_PDL if pdl else 0),
+        tile_n, split_k, _stream_handle(stream)))
     return out
 
 
 def quick_w4a16_gemm_raw(x_ptr: int, packed_ptr: int, M: int, N: int, K: int, group_size: int, y_ptr: int,
-                         stream_handle: int):
-    """Plain C-ABI call on raw device pointers (the entry point `quick_w4a16_gemm` of quick.h)."""
+                         stream_handle: int, flags: int = 0, tile_n: int = 0, split_k: int = 0, ldy: int = 0):
+    """Plain C-ABI call on raw device pointers (`quick_w4a16_gemm`, or `_ex` when any option is set)."""
+    if flags or tile_n or split_k or ldy:
+        _check("quick_w4a16_gemm_ex", _lib.quick_w4a16_gemm_ex(
+            ctypes.c_void_p(x_ptr), ctypes.c_void_p(packed_ptr), M, N, K, group_size, ctypes.c_void_p(y_ptr),
+            ldy or N, flags, tile_n, split_k, ctypes.c_void_p(stream_handle)))
+        return
     _check("quick_w4a16_gemm", _lib.quick_w4a16_gemm(ctypes.c_void_p(x_ptr), ctypes.c_void_p(packed_ptr), M, N, K,
                                                      group_size, ctypes.c_void_p(y_ptr),
                                                      ctypes.c_void_p(stream_handle)))
