@@ -17,9 +17,10 @@
 //               STAGES-deep mbarrier ring
 //   warp 1      TMEM allocator + MMA issuer (one thread): 4 x tcgen05.mma.kind::f16 per
 //               64-k stage, fp32 accumulation in TMEM (reading R4), tcgen05.commit -> mbarriers
-//   warps 2..9  dequantizers: one LDS.128 of 32 codes (own row) -> 4 x (LOP3 x4, HSUB2/HFMA2
-//               -> exact (q-z), HMUL2 by s) -> tcgen05.st.32x32b.x16 into the TMEM A ring;
-//               then the epilogue (tcgen05.ld -> fp16/fp32 -> Y), or for split-K the fp32
+//   warps 2..9  dequantizers, two groups of 4 taking alternate stages: per stage a thread
+//               (one TMEM lane = one weight row) does 2 x LDS.128 of 64 codes -> 8 x (LOP3 x4,
+//               HSUB2/HFMA2 -> exact (q-z), HMUL2 by s) -> tcgen05.st.32x32b.x32 into the TMEM
+//               A ring (software-pipelined against the next stage); then the epilogue (tcgen05.ld -> fp16/fp32 -> Y), or for split-K the fp32
 //               partial -> SMEM, cluster barrier, fixed-order DSMEM reduction (deterministic).
 // Split-K: the S CTAs of a (S,1,1) cluster share one (n-tile, m-tile) and split K (the
 // "split-k" knob of §5); partial sums stay fp32 (tolerance analysis).
@@ -179,10 +180,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
-      ptx::mbar_init(bar_empty + 8 * s, 8 + 1);  // 8 dequant warps + 1 MMA commit
+      ptx::mbar_init(bar_empty + 8 * s, 4 + 1);  // 4 dequant warps + 1 MMA commit
     }
     for (int a = 0; a < kAStages; ++a) {
-      ptx::mbar_init(bar_afull + 8 * a, 8);
+      ptx::mbar_init(bar_afull + 8 * a, 4);   // the 4 warps of a parity group
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
     ptx::mbar_init(bar_dfull, 1);
@@ -251,8 +252,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       int slot = 0, as = 0;
       uint32_t ph = 0, aph = 0;
       for (int it = 0; it < nst; ++it) {
-        ptx::mbar_wait(bar_full + 8 * slot, ph);     // X tile landed
-        ptx::mbar_wait(bar_afull + 8 * as, aph);     // A stage written by all 8 dequant warps
+        // A stage written by the 4 warps of its parity group; they waited on `full`, which
+        // also covers this stage's X tile, so one wait orders both operands
+        ptx::mbar_wait(bar_afull + 8 * as, aph);
         ptx::tc_fence_after();
         const uint32_t xaddr = sbase + C::X_OFF + slot * C::X_BYTES;
 #pragma unroll
@@ -270,39 +272,68 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     __syncwarp();
   } else {
     // ------------------------------------------------------------------ dequantizers
+    // Two groups of four warps take alternate stages (parity p); inside a group warp w owns
+    // TMEM lane quarter q = w % 4 (the only lanes it may access) and both 32-k chunks of the
+    // stage for its 32 rows.  Each warp is software-pipelined: the tcgen05.st of stage i
+    // completes while the warp loads and dequantizes stage i + 2.
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int h = (warp - 2) >> 2;       // which 32-k chunk of the 64-k stage
+    const int p = (warp - 2) >> 2;       // stage parity handled by this warp
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
-    int slot = 0, as = 0;
-    uint32_t ph = 0, aph = 0;
-    for (int it = 0; it < nst; ++it) {
-      ptx::mbar_wait(bar_full + 8 * slot, ph);
-      const int k0 = (kb + it) * kStageK;
-      const int gi = group_of(k0 + 32 * h) - group_of(k0);
-      const uint8_t* meta = smem + C::M_OFF + slot * kMetaStageBytes + gi * kMetaBytes;
-      const uint32_t sbits = reinterpret_cast<const uint16_t*>(meta)[r];
-      const uint32_t zbyte = meta[256 + (r >> 1)];
-      const uint4 wv = *reinterpret_cast<const uint4*>(smem + C::W_OFF + slot * kWStageBytes +
-                                                        h * (kWStageBytes / 2) + r * 16);
+    const uint8_t* wrow = smem + C::W_OFF + r * 16;
+    uint32_t a[32];
+    int it = p;
+    int slot = p % STAGES;
+    uint32_t ph = (uint32_t)(p / STAGES) & 1u;
+    auto load_dequant = [&](int i, int sl, uint32_t phase) {
+      ptx::mbar_wait(bar_full + 8 * sl, phase);
+      const int k0 = (kb + i) * kStageK;
+      const int g0 = group_of(k0);
+      const uint8_t* meta = smem + C::M_OFF + sl * kMetaStageBytes;
+      const uint8_t* meta1 = meta + (group_of(k0 + 32) - g0) * kMetaBytes;
+      const uint32_t s0 = reinterpret_cast<const uint16_t*>(meta)[r];
+      const uint32_t z0 = meta[256 + (r >> 1)];
+      const uint32_t s1 = reinterpret_cast<const uint16_t*>(meta1)[r];
+      const uint32_t z1 = meta1[256 + (r >> 1)];
+      const uint4 w0 = *reinterpret_cast<const uint4*>(wrow + sl * kWStageBytes);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(wrow + sl * kWStageBytes + kWStageBytes / 2);
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_empty + 8 * slot);
-      const DequantConsts dc = make_consts(sbits, (zbyte >> ((r & 1) * 4)) & 0xFu);
-      uint32_t a[16];
-      dequant_word(wv.x, dc, a + 0);
-      dequant_word(wv.y, dc, a + 4);
-      dequant_word(wv.z, dc, a + 8);
-      dequant_word(wv.w, dc, a + 12);
+      if (lane == 0) ptx::mbar_arrive(bar_empty + 8 * sl);   // smem of this stage consumed
+      const DequantConsts c0 = make_consts(s0, (z0 >> ((r & 1) * 4)) & 0xFu);
+      const DequantConsts c1 = make_consts(s1, (z1 >> ((r & 1) * 4)) & 0xFu);
+      dequant_word(w0.x, c0, a + 0);
+      dequant_word(w0.y, c0, a + 4);
+      dequant_word(w0.z, c0, a + 8);
+      dequant_word(w0.w, c0, a + 12);
+      dequant_word(w1.x, c1, a + 16);
+      dequant_word(w1.y, c1, a + 20);
+      dequant_word(w1.z, c1, a + 24);
+      dequant_word(w1.w, c1, a + 28);
+    };
+    auto advance2 = [&](int& sl, uint32_t& phase) {
+      sl += 2;
+      if (sl >= STAGES) {
+        sl -= STAGES;
+        phase ^= 1u;
+      }
+    };
+    if (it < nst) load_dequant(it, slot, ph);
+    while (it < nst) {
+      const int as = it & (kAStages - 1);
+      const uint32_t aph = (uint32_t)(it >> 2) & 1u;
       ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
       ptx::tc_fence_after();
-      ptx::tmem_st_32x32b_x16(tmem + tlane + as * kAColsPerStage + h * 16, a);
+      ptx::tmem_st_32x32b_x32(tmem + tlane + as * kAColsPerStage, a);
+      const int next = it + 2;
+      advance2(slot, ph);
+      if (next < nst) load_dequant(next, slot, ph);   // overlaps the TMEM store above
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
-      if (++slot == STAGES) { slot = 0; ph ^= 1u; }
-      if (++as == kAStages) { as = 0; aph ^= 1u; }
+      it = next;
     }
+    const int h = p;   // epilogue: this warp's half of the accumulator columns
     // ------------------------------------------------------------------ epilogue part 1
     constexpr int kColsPerWarp = BN / 2;
     const int j0 = h * kColsPerWarp;
@@ -600,54 +631,34 @@ int max_resident(int bn, int S) {
 
 struct Plan {
   int tile_n, split, ctas;
-  double cost;
 };
 
-// Cost model in SM cycles.  Per 64-k stage a CTA needs max(MMA, dequant)
-// cycles: MMA 4 x (BN / 2) (4096 fp16 MAC/clk/SM), dequant ~kDequantCycles for 8192 weights;
-// a wave of CTAs pays a fixed prologue/epilogue; split-K adds a DSMEM reduction; the chip
-// cannot beat HBM for the weights nor L2 for the X re-reads.
-constexpr double kDequantCycles = 110.0;
-constexpr double kFixedCycles = 2500.0;
-constexpr double kHbmBytesPerCycle = 3300.0;   // ~6.5 TB/s at ~1.9 GHz
-constexpr double kL2BytesPerCycle = 5500.0;
-constexpr double kDsmemBytesPerCycle = 18.0;
+int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
 
-Plan evaluate(int M, int N, int K, int G, int bn, int S) {
-  const int KT = K / quick::kStageK;
-  const int n_tiles = N / quick::kTileRows;
-  const int m_tiles = (M + bn - 1) / bn;
-  const int tiles = n_tiles * m_tiles;
-  const int resident = max_resident(bn, S);
-  const int waves = (tiles + resident - 1) / resident;
-  const int stages = (KT + S - 1) / S;
-  const double per_stage = std::max(2.0 * bn, kDequantCycles);
-  double t_cta = stages * per_stage + kFixedCycles;
-  if (S > 1) t_cta += 800.0 + (double)bn * quick::kTileRows * 4.0 * (S - 1) / S / kDsmemBytesPerCycle;
-  const double wbytes = (double)K * N / 2 + (double)(K / G) * N * 2.5;
-  const double xbytes = (double)n_tiles * M * K * 2;
-  const double cost = std::max({waves * t_cta, wbytes * m_tiles / kHbmBytesPerCycle + kFixedCycles,
-                                xbytes / kL2BytesPerCycle + kFixedCycles});
-  return Plan{bn, S, tiles * S, cost};
-}
-
+// Launch plan (tuned with tools/tune_plan.py on B200):
+//  - tokens per tile: the smallest MMA N covering M (weights are dequantized once per m-tile,
+//    so larger M uses the widest tile; M > 256 tiles the tokens by 256);
+//  - split-K: the largest S <= 8 such that all tiles x S CTAs are resident in one wave (TMEM
+//    and shared memory allow 2 CTAs/SM up to tile 128, 1 above; clusters are GPC-placed, so
+//    residency is queried, not computed) and every CTA keeps >= 4 stages of K.
 Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
+  (void)G;
   const int KT = K / quick::kStageK;
-  Plan best{0, 0, 0, 1e300};
-  for (int ti = 0; ti < 5; ++ti) {
-    const int bn = kTiles[ti];
-    if (force_tile > 0 && bn != force_tile) continue;
-    // candidate tiles: the smallest tile covering M, and (for larger M) one or two smaller
-    // tiles, which trade extra dequantization for fewer split-K partials
-    const int cover = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
-    if (force_tile <= 0 && (bn > cover || bn * 4 < cover)) continue;
-    for (int S = 1; S <= quick::kMaxSplit && S <= KT; ++S) {
-      if (force_split > 0 && S != force_split) continue;
-      Plan p = evaluate(M, N, K, G, bn, S);
-      if (p.cost < best.cost * 0.97) best = p;   // prefer the earlier (smaller S) on near-ties
+  const int tn = force_tile > 0 ? force_tile : cover_tile(M);
+  const int tiles = (N / quick::kTileRows) * ((M + tn - 1) / tn);
+  int S = 1;
+  if (force_split > 0) {
+    S = force_split;
+  } else {
+    const int per_sm = (quick::kDCol + tn <= 256) ? 2 : 1;
+    const int cap = per_sm * sm_count();
+    for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= KT / 4; ++s2) {
+      if (tiles * s2 > cap) break;
+      if (tiles > max_resident(tn, s2)) continue;
+      S = s2;
     }
   }
-  return best;
+  return Plan{tn, S, tiles * S};
 }
 
 template <int BN>
