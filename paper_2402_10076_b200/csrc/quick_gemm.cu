@@ -48,6 +48,8 @@ constexpr int kWStageBytes = kTileRows * kStageK / 2;  // 4 KiB of int4 codes pe
 constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-tile, group)
 constexpr int kMetaStageBytes = 2 * kMetaBytes;  // a 64-k stage touches <= 2 groups (G % 32 == 0)
 constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable clusters)
+constexpr int kTraceStages = 256; // debug tracing: stages recorded per traced CTA
+constexpr int kTraceStride = 8 + 7 * kTraceStages;
 
 template <int BN>
 struct Cfg {
@@ -149,7 +151,8 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const uint8_t* __restrict__ packed, void* __restrict__ Y, int M, int N,
-                          int K, int G, int g_shift, int ldy, int flags) {
+                          int K, int G, int g_shift, int ldy, int flags,
+                          unsigned long long* __restrict__ trace) {
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -195,6 +198,14 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  // debug tracing (tools/trace_gemm.py; null in production): clock64 stamps per stage
+  unsigned long long* tr = nullptr;
+  if (trace != nullptr && blockIdx.z == 0 && blockIdx.y < 2)
+    tr = trace + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * kTraceStride;
+  auto stamp = [&](int ev, int i) {
+    if (tr != nullptr && i < kTraceStages) tr[8 + ev * kTraceStages + i] = clock64();
+  };
+  if (tr != nullptr && threadIdx.x == 0) tr[0] = clock64();
   // let the next kernel in the stream launch its prologue early (PDL); it still waits for
   // this grid's completion before touching anything this grid writes
   ptx::griddep_launch_dependents();
@@ -218,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       int slot = 0;
       uint32_t ph = 0;
       for (int it = 0; it < nst; ++it) {
+        stamp(0, it);
         if (it >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
         const int k0 = (kb + it) * kStageK;
         const int g0 = group_of(k0);
@@ -241,6 +253,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         } else if (it >= pre) {
           ptx::tma_load_2d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, k0, m0, full, pol_x);
         }
+        stamp(1, it);
         if (++slot == STAGES) { slot = 0; ph ^= 1u; }
       }
     }
@@ -255,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         // A stage written by the 4 warps of its parity group; they waited on `full`, which
         // also covers this stage's X tile, so one wait orders both operands
         ptx::mbar_wait(bar_afull + 8 * as, aph);
+        stamp(5, it);
         ptx::tc_fence_after();
         const uint32_t xaddr = sbase + C::X_OFF + slot * C::X_BYTES;
 #pragma unroll
@@ -264,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         }
         ptx::mma_commit(bar_empty + 8 * slot);   // X slot free once these MMAs complete
         ptx::mma_commit(bar_aempty + 8 * as);    // A stage free
+        stamp(6, it);
         if (++slot == STAGES) { slot = 0; ph ^= 1u; }
         if (++as == kAStages) { as = 0; aph ^= 1u; }
       }
@@ -285,8 +300,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     int it = p;
     int slot = p % STAGES;
     uint32_t ph = (uint32_t)(p / STAGES) & 1u;
+    const bool tw = (q == 0 && lane == 0);   // this warp's lane 0 stamps the trace
     auto load_dequant = [&](int i, int sl, uint32_t phase) {
       ptx::mbar_wait(bar_full + 8 * sl, phase);
+      if (tw) stamp(2, i);
       const int k0 = (kb + i) * kStageK;
       const int g0 = group_of(k0);
       const uint8_t* meta = smem + C::M_OFF + sl * kMetaStageBytes;
@@ -322,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       const int as = it & (kAStages - 1);
       const uint32_t aph = (uint32_t)(it >> 2) & 1u;
       ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+      if (tw) stamp(3, it);
       ptx::tc_fence_after();
       ptx::tmem_st_32x32b_x32(tmem + tlane + as * kAColsPerStage, a);
       const int next = it + 2;
@@ -331,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
+      if (tw) stamp(4, it);
       it = next;
     }
     const int h = p;   // epilogue: this warp's half of the accumulator columns
@@ -342,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       ptx::mbar_wait(bar_dfull, 0);
       ptx::tc_fence_after();
     }
+    if (tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
     float* part = reinterpret_cast<float*>(smem);  // [BN][128] fp32 (split-K only)
 #pragma unroll 1
     for (int jc = 0; jc < kColsPerWarp; jc += 8) {
@@ -420,6 +440,13 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (tr != nullptr && threadIdx.x == 0) {
+    tr[2] = clock64();
+    tr[3] = (unsigned long long)nst;
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[4] = smid;
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, C::TMEM_COLS);
@@ -493,6 +520,7 @@ __global__ void quick_gather_columns_kernel(const uint4* __restrict__ src, uint4
 namespace {
 
 thread_local int g_last_cuda_error = 0;
+unsigned long long* g_trace = nullptr;   // debug tracing buffer (quick_debug_set_trace)
 
 quick_status_t cuda_fail(cudaError_t e) {
   g_last_cuda_error = (int)e;
@@ -696,7 +724,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, i
   }
   const uint8_t* pk = static_cast<const uint8_t*>(packed);
   e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN>, tmap, pk, Y, M, N, K, G, g_shift,
-                         ldy, flags);
+                         ldy, flags, g_trace);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
 }
@@ -708,6 +736,12 @@ inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintp
 extern "C" {
 
 int quick_last_cuda_error(void) { return g_last_cuda_error; }
+
+// Debug only (not part of quick.h): device buffer of 16 * (8 + 7 * 256) uint64 clock stamps
+// written by the next launches for CTAs with blockIdx.z == 0 and blockIdx.y < 2; NULL disables.
+void quick_debug_set_trace(void* device_buffer) {
+  g_trace = static_cast<unsigned long long*>(device_buffer);
+}
 
 quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* split_k,
                                int* num_ctas) {

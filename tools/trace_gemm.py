@@ -1,0 +1,56 @@
+"""Per-stage clock64 trace of the W4A16 kernel pipeline (debug hook quick_debug_set_trace).
+usage: python tools/trace_gemm.py M N K [tile_n split_k]"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2402_10076_b200 import quick  # noqa: E402
+
+M, N, K = (int(v) for v in sys.argv[1:4])
+tn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+sk = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+G, TS, STRIDE = 128, 256, 8 + 7 * 256
+lib = quick.raw_library()
+lib.quick_debug_set_trace.argtypes = [ctypes.c_void_p]
+p = synth.make_problem(0, M, N, K, G)
+blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).cuda()
+copies = [blob.clone() for _ in range(max(2, int(3e8 // blob.numel())))]
+x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
+y = torch.empty((M, N), device="cuda", dtype=torch.float16)
+tr = torch.zeros(16 * STRIDE, dtype=torch.int64, device="cuda")
+for i in range(3):
+    quick.quick_w4a16_gemm(x, copies[i], N, K, G, out=y, tile_n=tn, split_k=sk)
+torch.cuda.synchronize()
+lib.quick_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
+quick.quick_w4a16_gemm(x, copies[-1], N, K, G, out=y, tile_n=tn, split_k=sk)
+torch.cuda.synchronize()
+lib.quick_debug_set_trace(ctypes.c_void_p(0))
+t = tr.cpu().numpy().reshape(16, STRIDE)
+print("plan", quick.quick_gemm_plan(M, N, K, G), "tile", tn, "split", sk)
+names = ["P_before_empty", "P_issued", "D_full", "D_aempty_ok", "D_afull_arrived", "M_afull_ok", "M_committed"]
+for c in range(16):
+    row = t[c]
+    if row[0] == 0:
+        continue
+    nst = int(row[3])
+    n = min(nst, TS)
+    ev = row[8:].reshape(7, TS)[:, :n].astype(np.int64) - int(row[0])
+    print(f"CTA {c} sm {row[4]} nst {nst}: setup->end {int(row[2]) - int(row[0])} cyc, dfull at {int(row[1]) - int(row[0])}")
+    if c < 2:
+        for i in list(range(min(n, 6))) + list(range(max(6, n - 3), n)):
+            print("  it", i, " ".join(f"{nm}={ev[j, i]}" for j, nm in enumerate(names)))
+    if n > 8:
+        mid = slice(4, n - 2)
+        d = lambda a: float(np.mean(np.diff(a[mid])))
+        print("   per-stage interval: " + " ".join(f"{nm}={d(ev[j]):.0f}" for j, nm in enumerate(names)))
+        print("   latencies: issue->full %.0f  full->aempty %.0f  aempty->afull %.0f  afull->mma %.0f  mma issue %.0f" % (
+            np.mean(ev[2, mid] - ev[1, mid]), np.mean(ev[3, mid] - ev[2, mid]), np.mean(ev[4, mid] - ev[3, mid]),
+            np.mean(ev[5, mid] - ev[4, mid]), np.mean(ev[6, mid] - ev[5, mid])))
+        # MMA commit (stage i) -> dequant sees aempty for stage i + 4
+        if n > 12:
+            print("   commit(i)->aempty(i+4) %.0f" % np.mean(ev[3, 8:n - 2] - ev[6, 4:n - 6]))
