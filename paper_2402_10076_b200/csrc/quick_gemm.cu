@@ -217,73 +217,82 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
-    if (lane == 0) {
-      const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
-      const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
-      const uint8_t* wbase = packed + (size_t)t * C32 * kTileRows * 16;
-      const uint8_t* mbase = packed + (size_t)K * N / 2 + (size_t)t * NG * kMetaBytes;
-      // Weights and metadata are read-only for this call: their bulk copies may be issued
-      // before the programmatic grid dependency resolves; X may be produced by the previous
-      // kernel, so its TMA waits for it (PDL).
-      const int pre = pdl ? (nst < STAGES ? nst : STAGES) : 0;
-      int slot = 0;
-      uint32_t ph = 0;
-      for (int it = 0; it < nst; ++it) {
-        stamp(0, it);
-        if (it >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
-        const int k0 = (kb + it) * kStageK;
-        const int g0 = group_of(k0);
-        const int g1 = group_of(k0 + kStageK - 1);
-        const uint32_t meta_bytes = (uint32_t)(g1 - g0 + 1) * kMetaBytes;
-        const uint32_t full = bar_full + 8 * slot;
+    // The whole warp runs the (warp-uniform) loop; one elected lane issues the copies, so the
+    // addresses stay in uniform registers and no per-lane waterfall is generated.
+    const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
+    const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
+    const uint8_t* wptr = packed + ((size_t)t * C32 + (size_t)kb * (kStageK / 32)) * kTileRows * 16;
+    const uint8_t* mbase = packed + (size_t)K * N / 2 + (size_t)t * NG * kMetaBytes;
+    // Weights and metadata are read-only for this call: their bulk copies may be issued
+    // before the programmatic grid dependency resolves; X may be produced by the previous
+    // kernel, so its TMA waits for it (PDL).
+    const int pre = pdl ? (nst < STAGES ? nst : STAGES) : 0;
+    int slot = 0;
+    uint32_t ph = 0;
+    int k0 = kb * kStageK;
+    for (int it = 0; it < nst; ++it) {
+      if (lane == 0) stamp(0, it);
+      if (it >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
+      const int g0 = group_of(k0);
+      const uint32_t meta_bytes = (uint32_t)(group_of(k0 + kStageK - 1) - g0 + 1) * kMetaBytes;
+      const uint32_t full = bar_full + 8 * slot;
+      if (ptx::elect_one()) {
         ptx::mbar_arrive_expect_tx(full, C::X_BYTES + kWStageBytes + meta_bytes);
-        ptx::bulk_load_hint(sbase + C::W_OFF + slot * kWStageBytes,
-                            wbase + (size_t)(k0 / 32) * kTileRows * 16, kWStageBytes, full, pol_w);
-        ptx::bulk_load_hint(sbase + C::M_OFF + slot * kMetaStageBytes,
-                            mbase + (size_t)g0 * kMetaBytes, meta_bytes, full, pol_w);
-        if (it == pre - 1 || (pre == 0 && it == 0)) {
-          if (pdl) ptx::griddep_wait();
-          // X loads of the stages issued so far (weights went first)
-          int s2 = 0;
-          for (int j = 0; j <= it; ++j) {
-            ptx::tma_load_2d_hint(sbase + C::X_OFF + s2 * C::X_BYTES, &tmap_x, (kb + j) * kStageK, m0,
-                                  bar_full + 8 * s2, pol_x);
-            s2 = (s2 + 1 == STAGES) ? 0 : s2 + 1;
-          }
-        } else if (it >= pre) {
+        ptx::bulk_load_hint(sbase + C::W_OFF + slot * kWStageBytes, wptr, kWStageBytes, full, pol_w);
+        ptx::bulk_load_hint(sbase + C::M_OFF + slot * kMetaStageBytes, mbase + (size_t)g0 * kMetaBytes,
+                            meta_bytes, full, pol_w);
+        if (it >= pre && !(pre == 0 && it == 0)) {
           ptx::tma_load_2d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, k0, m0, full, pol_x);
+        } else if (it == (pre > 0 ? pre - 1 : 0)) {
+          if (pdl) ptx::griddep_wait();
+          for (int j = 0; j <= it; ++j)   // X of the stages issued so far (weights went first)
+            ptx::tma_load_2d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, (kb + j) * kStageK, m0,
+                                  bar_full + 8 * j, pol_x);
         }
-        stamp(1, it);
-        if (++slot == STAGES) { slot = 0; ph ^= 1u; }
       }
+      __syncwarp();
+      if (lane == 0) stamp(1, it);
+      if (++slot == STAGES) {
+        slot = 0;
+        ph ^= 1u;
+      }
+      k0 += kStageK;
+      wptr += kWStageBytes;
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = instr_desc<BN>();
-      int slot = 0, as = 0;
-      uint32_t ph = 0, aph = 0;
-      for (int it = 0; it < nst; ++it) {
-        // A stage written by the 4 warps of its parity group; they waited on `full`, which
-        // also covers this stage's X tile, so one wait orders both operands
-        ptx::mbar_wait(bar_afull + 8 * as, aph);
-        stamp(5, it);
-        ptx::tc_fence_after();
-        const uint32_t xaddr = sbase + C::X_OFF + slot * C::X_BYTES;
+    // Warp-uniform loop; one elected lane issues the MMAs and the commits (a commit tracks
+    // the async tcgen05 ops of the thread that issues it, so the same lane does both).
+    constexpr uint32_t idesc = instr_desc<BN>();
+    const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
+    int slot = 0, as = 0;
+    uint32_t aph = 0;
+    for (int it = 0; it < nst; ++it) {
+      // A stage written by the 4 warps of its parity group; they waited on `full`, which
+      // also covers this stage's X tile, so one wait orders both operands
+      ptx::mbar_wait(bar_afull + 8 * as, aph);
+      if (lane == 0) stamp(5, it);
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        // descriptor start address advances 16 B units: X stage slot, then 32 B per K=16 step
+        const uint64_t dslot = desc0 + (uint64_t)((slot * C::X_BYTES) >> 4);
+        const uint32_t a_col = tmem + as * kAColsPerStage;
 #pragma unroll
-        for (int kk = 0; kk < kStageK / 16; ++kk) {
-          ptx::mma_f16_ts(tmem + kDCol, tmem + as * kAColsPerStage + kk * 8,
-                          sw128_desc(xaddr + kk * 32), idesc, (it | kk) != 0 ? 1u : 0u);
-        }
+        for (int kk = 0; kk < kStageK / 16; ++kk)
+          ptx::mma_f16_ts(tmem + kDCol, a_col + kk * 8, dslot + (uint64_t)(kk * 2), idesc,
+                          (it | kk) != 0 ? 1u : 0u);
         ptx::mma_commit(bar_empty + 8 * slot);   // X slot free once these MMAs complete
         ptx::mma_commit(bar_aempty + 8 * as);    // A stage free
-        stamp(6, it);
-        if (++slot == STAGES) { slot = 0; ph ^= 1u; }
-        if (++as == kAStages) { as = 0; aph ^= 1u; }
       }
-      ptx::mma_commit(bar_dfull);
+      __syncwarp();
+      if (lane == 0) stamp(6, it);
+      if (++slot == STAGES) slot = 0;
+      if (++as == kAStages) {
+        as = 0;
+        aph ^= 1u;
+      }
     }
+    if (ptx::elect_one()) ptx::mma_commit(bar_dfull);
     __syncwarp();
   } else {
     // ------------------------------------------------------------------ dequantizers
