@@ -40,26 +40,34 @@ namespace quick {
 
 constexpr int kThreads = 320;     // 10 warps
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
-constexpr int kStageK = 64;       // k per pipeline stage (4 MMAs of K=16)
-constexpr int kAStages = 4;       // depth of the TMEM A-operand ring
-constexpr int kAColsPerStage = 32;              // 64 fp16 of k = 32 x 32-bit TMEM columns
-constexpr int kDCol = kAStages * kAColsPerStage;  // accumulator columns start here
-constexpr int kWStageBytes = kTileRows * kStageK / 2;  // 4 KiB of int4 codes per stage
+constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
+constexpr int kAStages = 2;       // depth of the TMEM A-operand ring
+constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
+constexpr int kDCol = kAStages * kAColsPerStage;  // accumulator columns start here (128)
+constexpr int kChunkBytes = kTileRows * 16;       // 32 k x 128 rows of int4 = one 2 KiB chunk
 constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-tile, group)
-constexpr int kMetaStageBytes = 2 * kMetaBytes;  // a 64-k stage touches <= 2 groups (G % 32 == 0)
 constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable clusters)
 constexpr int kTraceStages = 256; // debug tracing: stages recorded per traced CTA
 constexpr int kTraceStride = 8 + 7 * kTraceStages;
 
+// Per tile width BN (tokens per MMA): KL = k per load stage (one bulk copy of KL x 64 B of
+// weights, one bulk copy of the groups' metadata, one 3-D TMA of the [KL/64][BN][64] X tile),
+// STAGES = depth of the load ring.  Few, large async copies per byte: each TMA/bulk issue
+// costs ~150 SM cycles on B200 (measured with tools/trace_gemm.py).
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = BN <= 16 ? 12 : BN <= 32 ? 10 : BN <= 64 ? 7 : BN <= 128 ? 5 : 4;
-  static constexpr int X_BYTES = BN * kStageK * 2;  // [BN][64] fp16, 128-B rows, SW128
+  static constexpr int KL = BN <= 32 ? 256 : 128;
+  static constexpr int APL = KL / kKA;              // A stages per load stage
+  static constexpr int STAGES = BN <= 16 ? 3 : BN <= 32 ? 3 : BN <= 64 ? 4 : 2;
+  static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
+  static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
+  static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
+  static constexpr int M_BYTES = ((KL / 32 + 1) * kMetaBytes + 15) & ~15;  // worst case G = 32
   static constexpr int X_OFF = 0;
   static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
-  static constexpr int M_OFF = W_OFF + STAGES * kWStageBytes;
-  static constexpr int BAR_OFF = (M_OFF + STAGES * kMetaStageBytes + 7) & ~7;
-  // barriers: full[STAGES], empty[STAGES], afull[4], aempty[4], dfull
+  static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
+  static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
+  // barriers: full[STAGES], empty[STAGES], afull[kAStages], aempty[kAStages], dfull
   static constexpr int NUM_BARS = 2 * STAGES + 2 * kAStages + 1;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;
   static constexpr int USED = HOLD_OFF + 16;
@@ -70,6 +78,7 @@ struct Cfg {
   static constexpr int MIN_SMEM = (228 * 1024) / (MAX_CTAS_PER_SM + 1) + 1024;
   static constexpr int SMEM_BYTES = (USED + 1024 > MIN_SMEM ? USED + 1024 : MIN_SMEM);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
+  static_assert(KL % kKA == 0, "load stage = whole A stages");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // split-K partial tile [BN][128] fp32 reuses the pipeline buffers once the mainloop is done
   static_assert(BN * kTileRows * 4 <= BAR_OFF, "split-K partial must fit in the pipeline smem");
@@ -155,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
                           unsigned long long* __restrict__ trace) {
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES;
+  constexpr int APL = C::APL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -166,12 +176,19 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   const int split = blockIdx.x;
   const int t = blockIdx.y;           // n-tile
   const int m0 = blockIdx.z * BN;     // first token of this tile
-  const int KT = K / kStageK;
-  const int kb = (int)(((long long)split * KT) / S);
-  const int ke = (int)(((long long)(split + 1) * KT) / S);
-  const int nst = ke - kb;
+  // K is split over the cluster in whole A stages (128 k; the last one of K may hold 64)
+  const int NA = (K + kKA - 1) / kKA;
+  const int a_begin = (int)(((long long)split * NA) / S);
+  const int na = (int)(((long long)(split + 1) * NA) / S) - a_begin;   // A stages of this CTA
+  const int k_begin = a_begin * kKA;
+  const int k_end = min(k_begin + na * kKA, K);
+  const int nl = (na + APL - 1) / APL;                                   // load stages
   const int C32 = K / 32;
   const int NG = K / G;
+  const bool out_fp32 = (flags & QUICK_FLAG_OUT_F32) != 0;
+  const bool pdl = (flags & QUICK_FLAG_PDL) != 0;
+  // group index of k: shift when G is a power of two, division otherwise
+  auto group_of = [&](int k) { return g_shift >= 0 ? (k >> g_shift) : (k / G); };
 
   const uint32_t bar_full = sbase + C::BAR_OFF;
   const uint32_t bar_empty = bar_full + 8 * STAGES;
@@ -183,10 +200,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
-      ptx::mbar_init(bar_empty + 8 * s, 4 + 1);  // 4 dequant warps + 1 MMA commit
+      ptx::mbar_init(bar_empty + 8 * s, 8 + 1);  // 8 dequant warps + 1 MMA commit
     }
     for (int a = 0; a < kAStages; ++a) {
-      ptx::mbar_init(bar_afull + 8 * a, 4);   // the 4 warps of a parity group
+      ptx::mbar_init(bar_afull + 8 * a, 8);      // all 8 dequant warps write each A stage
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
     ptx::mbar_init(bar_dfull, 1);
@@ -210,54 +227,50 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   // this grid's completion before touching anything this grid writes
   ptx::griddep_launch_dependents();
 
-  const bool out_fp32 = (flags & QUICK_FLAG_OUT_F32) != 0;
-  const bool pdl = (flags & QUICK_FLAG_PDL) != 0;
-  // group index of k: shift when G is a power of two, division otherwise
-  auto group_of = [&](int k) { return g_shift >= 0 ? (k >> g_shift) : (k / G); };
-
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     // The whole warp runs the (warp-uniform) loop; one elected lane issues the copies, so the
     // addresses stay in uniform registers and no per-lane waterfall is generated.
     const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
-    const uint8_t* wptr = packed + ((size_t)t * C32 + (size_t)kb * (kStageK / 32)) * kTileRows * 16;
+    const uint8_t* wbase = packed + (size_t)t * C32 * kChunkBytes;
     const uint8_t* mbase = packed + (size_t)K * N / 2 + (size_t)t * NG * kMetaBytes;
     // Weights and metadata are read-only for this call: their bulk copies may be issued
     // before the programmatic grid dependency resolves; X may be produced by the previous
     // kernel, so its TMA waits for it (PDL).
-    const int pre = pdl ? (nst < STAGES ? nst : STAGES) : 0;
+    const int pre = pdl ? (nl < STAGES ? nl : STAGES) : 0;
     int slot = 0;
     uint32_t ph = 0;
-    int k0 = kb * kStageK;
-    for (int it = 0; it < nst; ++it) {
-      if (lane == 0) stamp(0, it);
-      if (it >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
-      const int g0 = group_of(k0);
-      const uint32_t meta_bytes = (uint32_t)(group_of(k0 + kStageK - 1) - g0 + 1) * kMetaBytes;
+    for (int l = 0; l < nl; ++l) {
+      const int kl0 = k_begin + l * C::KL;
+      const int kv = min(C::KL, k_end - kl0);          // valid k in this load stage
+      if (lane == 0) stamp(0, l);
+      if (l >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
+      const int g0 = group_of(kl0);
+      const uint32_t meta_bytes = (uint32_t)(group_of(kl0 + kv - 1) - g0 + 1) * kMetaBytes;
       const uint32_t full = bar_full + 8 * slot;
       if (ptx::elect_one()) {
-        ptx::mbar_arrive_expect_tx(full, C::X_BYTES + kWStageBytes + meta_bytes);
-        ptx::bulk_load_hint(sbase + C::W_OFF + slot * kWStageBytes, wptr, kWStageBytes, full, pol_w);
-        ptx::bulk_load_hint(sbase + C::M_OFF + slot * kMetaStageBytes, mbase + (size_t)g0 * kMetaBytes,
+        ptx::mbar_arrive_expect_tx(full, C::X_BYTES + (uint32_t)kv * 64u + meta_bytes);
+        ptx::bulk_load_hint(sbase + C::W_OFF + slot * C::W_BYTES,
+                            wbase + (size_t)(kl0 / 32) * kChunkBytes, (uint32_t)kv * 64u, full, pol_w);
+        ptx::bulk_load_hint(sbase + C::M_OFF + slot * C::M_BYTES, mbase + (size_t)g0 * kMetaBytes,
                             meta_bytes, full, pol_w);
-        if (it >= pre && !(pre == 0 && it == 0)) {
-          ptx::tma_load_2d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, k0, m0, full, pol_x);
-        } else if (it == (pre > 0 ? pre - 1 : 0)) {
+        if (l >= pre && !(pre == 0 && l == 0)) {
+          ptx::tma_load_3d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, 0, m0, kl0 / 64, full,
+                                pol_x);
+        } else if (l == (pre > 0 ? pre - 1 : 0)) {
           if (pdl) ptx::griddep_wait();
-          for (int j = 0; j <= it; ++j)   // X of the stages issued so far (weights went first)
-            ptx::tma_load_2d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, (kb + j) * kStageK, m0,
-                                  bar_full + 8 * j, pol_x);
+          for (int j = 0; j <= l; ++j)   // X of the stages issued so far (weights went first)
+            ptx::tma_load_3d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, 0, m0,
+                                  (k_begin + j * C::KL) / 64, bar_full + 8 * j, pol_x);
         }
       }
       __syncwarp();
-      if (lane == 0) stamp(1, it);
+      if (lane == 0) stamp(1, l);
       if (++slot == STAGES) {
         slot = 0;
         ph ^= 1u;
       }
-      k0 += kStageK;
-      wptr += kWStageBytes;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
@@ -265,28 +278,36 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     // the async tcgen05 ops of the thread that issues it, so the same lane does both).
     constexpr uint32_t idesc = instr_desc<BN>();
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
-    int slot = 0, as = 0;
+    int slot = 0, sub = 0, as = 0;
     uint32_t aph = 0;
-    for (int it = 0; it < nst; ++it) {
-      // A stage written by the 4 warps of its parity group; they waited on `full`, which
-      // also covers this stage's X tile, so one wait orders both operands
+    for (int a = 0; a < na; ++a) {
+      // A stage written by all 8 dequant warps; they waited on `full`, which also covers the
+      // X tile of this load stage, so one wait orders both operands
       ptx::mbar_wait(bar_afull + 8 * as, aph);
-      if (lane == 0) stamp(5, it);
+      if (lane == 0) stamp(5, a);
       ptx::tc_fence_after();
+      const int kv = min(kKA, k_end - (k_begin + a * kKA));   // 128, or 64 at the end of K
       if (ptx::elect_one()) {
-        // descriptor start address advances 16 B units: X stage slot, then 32 B per K=16 step
-        const uint64_t dslot = desc0 + (uint64_t)((slot * C::X_BYTES) >> 4);
         const uint32_t a_col = tmem + as * kAColsPerStage;
+        // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
+        const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES + sub * 2 * C::X_SUB) >> 4);
 #pragma unroll
-        for (int kk = 0; kk < kStageK / 16; ++kk)
-          ptx::mma_f16_ts(tmem + kDCol, a_col + kk * 8, dslot + (uint64_t)(kk * 2), idesc,
-                          (it | kk) != 0 ? 1u : 0u);
-        ptx::mma_commit(bar_empty + 8 * slot);   // X slot free once these MMAs complete
-        ptx::mma_commit(bar_aempty + 8 * as);    // A stage free
+        for (int kk = 0; kk < kKA / 16; ++kk) {
+          if (kk * 16 < kv)
+            ptx::mma_f16_ts(tmem + kDCol, a_col + kk * 8,
+                            dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
+                            (a | kk) != 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
+        if (sub == APL - 1 || a == na - 1)
+          ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage consumed
       }
       __syncwarp();
-      if (lane == 0) stamp(6, it);
-      if (++slot == STAGES) slot = 0;
+      if (lane == 0) stamp(6, a);
+      if (++sub == APL || a == na - 1) {
+        sub = 0;
+        if (++slot == STAGES) slot = 0;
+      }
       if (++as == kAStages) {
         as = 0;
         aph ^= 1u;
@@ -296,77 +317,83 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     __syncwarp();
   } else {
     // ------------------------------------------------------------------ dequantizers
-    // Two groups of four warps take alternate stages (parity p); inside a group warp w owns
-    // TMEM lane quarter q = w % 4 (the only lanes it may access) and both 32-k chunks of the
-    // stage for its 32 rows.  Each warp is software-pipelined: the tcgen05.st of stage i
-    // completes while the warp loads and dequantizes stage i + 2.
+    // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access) and k-half h of
+    // every 128-k A stage: per stage a thread (one TMEM lane = one weight row) loads 2 x 16 B
+    // = 64 codes, dequantizes them and writes 32 TMEM columns with one tcgen05.st.  The warp
+    // is software-pipelined: the tcgen05.st of stage a completes while it loads and
+    // dequantizes stage a + 1.
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int p = (warp - 2) >> 2;       // stage parity handled by this warp
+    const int h = (warp - 2) >> 2;       // k-half of each A stage handled by this warp
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
-    const uint8_t* wrow = smem + C::W_OFF + r * 16;
-    uint32_t a[32];
-    int it = p;
-    int slot = p % STAGES;
-    uint32_t ph = (uint32_t)(p / STAGES) & 1u;
+    const uint8_t* wrow = smem + C::W_OFF + h * 2 * kChunkBytes + r * 16;
     const bool tw = (q == 0 && lane == 0);   // this warp's lane 0 stamps the trace
-    auto load_dequant = [&](int i, int sl, uint32_t phase) {
-      ptx::mbar_wait(bar_full + 8 * sl, phase);
-      if (tw) stamp(2, i);
-      const int k0 = (kb + i) * kStageK;
-      const int g0 = group_of(k0);
-      const uint8_t* meta = smem + C::M_OFF + sl * kMetaStageBytes;
-      const uint8_t* meta1 = meta + (group_of(k0 + 32) - g0) * kMetaBytes;
-      const uint32_t s0 = reinterpret_cast<const uint16_t*>(meta)[r];
-      const uint32_t z0 = meta[256 + (r >> 1)];
-      const uint32_t s1 = reinterpret_cast<const uint16_t*>(meta1)[r];
-      const uint32_t z1 = meta1[256 + (r >> 1)];
-      const uint4 w0 = *reinterpret_cast<const uint4*>(wrow + sl * kWStageBytes);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(wrow + sl * kWStageBytes + kWStageBytes / 2);
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_empty + 8 * sl);   // smem of this stage consumed
-      const DequantConsts c0 = make_consts(s0, (z0 >> ((r & 1) * 4)) & 0xFu);
-      const DequantConsts c1 = make_consts(s1, (z1 >> ((r & 1) * 4)) & 0xFu);
-      dequant_word(w0.x, c0, a + 0);
-      dequant_word(w0.y, c0, a + 4);
-      dequant_word(w0.z, c0, a + 8);
-      dequant_word(w0.w, c0, a + 12);
-      dequant_word(w1.x, c1, a + 16);
-      dequant_word(w1.y, c1, a + 20);
-      dequant_word(w1.z, c1, a + 24);
-      dequant_word(w1.w, c1, a + 28);
-    };
-    auto advance2 = [&](int& sl, uint32_t& phase) {
-      sl += 2;
-      if (sl >= STAGES) {
-        sl -= STAGES;
-        phase ^= 1u;
+    uint32_t a_regs[32];
+    // pipeline position of the A stage being loaded
+    int slot = 0, sub = 0;
+    uint32_t ph = 0;
+    auto load_dequant = [&](int a) {
+      const int kl0 = k_begin + (a - sub) * kKA;          // first k of this load stage
+      const int ka = k_begin + a * kKA + 64 * h;          // first k of this warp's half
+      if (sub == 0 || a == 0) ptx::mbar_wait(bar_full + 8 * slot, ph);
+      if (tw) stamp(2, a);
+      if (ka < k_end) {
+        const int g0 = group_of(kl0);
+        const uint8_t* meta = smem + C::M_OFF + slot * C::M_BYTES;
+        const uint8_t* meta0 = meta + (group_of(ka) - g0) * kMetaBytes;
+        const uint8_t* meta1 = meta + (group_of(ka + 32) - g0) * kMetaBytes;
+        const uint32_t s0 = reinterpret_cast<const uint16_t*>(meta0)[r];
+        const uint32_t z0 = meta0[256 + (r >> 1)];
+        const uint32_t s1 = reinterpret_cast<const uint16_t*>(meta1)[r];
+        const uint32_t z1 = meta1[256 + (r >> 1)];
+        const uint8_t* wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
+        const uint4 w0 = *reinterpret_cast<const uint4*>(wp);
+        const uint4 w1 = *reinterpret_cast<const uint4*>(wp + kChunkBytes);
+        __syncwarp();
+        if ((sub == APL - 1 || a == na - 1) && lane == 0) ptx::mbar_arrive(bar_empty + 8 * slot);
+        const DequantConsts c0 = make_consts(s0, (z0 >> ((r & 1) * 4)) & 0xFu);
+        const DequantConsts c1 = make_consts(s1, (z1 >> ((r & 1) * 4)) & 0xFu);
+        dequant_word(w0.x, c0, a_regs + 0);
+        dequant_word(w0.y, c0, a_regs + 4);
+        dequant_word(w0.z, c0, a_regs + 8);
+        dequant_word(w0.w, c0, a_regs + 12);
+        dequant_word(w1.x, c1, a_regs + 16);
+        dequant_word(w1.y, c1, a_regs + 20);
+        dequant_word(w1.z, c1, a_regs + 24);
+        dequant_word(w1.w, c1, a_regs + 28);
+      } else {
+        __syncwarp();
+        if ((sub == APL - 1 || a == na - 1) && lane == 0) ptx::mbar_arrive(bar_empty + 8 * slot);
+      }
+      if (++sub == APL || a == na - 1) {
+        sub = 0;
+        if (++slot == STAGES) {
+          slot = 0;
+          ph ^= 1u;
+        }
       }
     };
-    if (it < nst) load_dequant(it, slot, ph);
-    while (it < nst) {
-      const int as = it & (kAStages - 1);
-      const uint32_t aph = (uint32_t)(it >> 2) & 1u;
+    if (na > 0) load_dequant(0);
+    for (int a = 0; a < na; ++a) {
+      const int as = a & (kAStages - 1);
+      const uint32_t aph = (uint32_t)(a / kAStages) & 1u;
+      const bool valid = (k_begin + a * kKA + 64 * h) < k_end;
       ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
-      if (tw) stamp(3, it);
+      if (tw) stamp(3, a);
       ptx::tc_fence_after();
-      ptx::tmem_st_32x32b_x32(tmem + tlane + as * kAColsPerStage, a);
-      const int next = it + 2;
-      advance2(slot, ph);
-      if (next < nst) load_dequant(next, slot, ph);   // overlaps the TMEM store above
+      if (valid) ptx::tmem_st_32x32b_x32(tmem + tlane + as * kAColsPerStage + h * 32, a_regs);
+      if (a + 1 < na) load_dequant(a + 1);   // overlaps the TMEM store above
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
-      if (tw) stamp(4, it);
-      it = next;
+      if (tw) stamp(4, a);
     }
-    const int h = p;   // epilogue: this warp's half of the accumulator columns
     // ------------------------------------------------------------------ epilogue part 1
     constexpr int kColsPerWarp = BN / 2;
     const int j0 = h * kColsPerWarp;
     const int n = t * kTileRows + r;
-    if (nst > 0) {
+    if (na > 0) {
       ptx::mbar_wait(bar_dfull, 0);
       ptx::tc_fence_after();
     }
@@ -375,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
 #pragma unroll 1
     for (int jc = 0; jc < kColsPerWarp; jc += 8) {
       uint32_t v[8];
-      if (nst > 0) {
+      if (na > 0) {
         ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + j0 + jc, v);
         ptx::tmem_wait_ld();
       } else {
@@ -451,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   __syncthreads();
   if (tr != nullptr && threadIdx.x == 0) {
     tr[2] = clock64();
-    tr[3] = (unsigned long long)nst;
+    tr[3] = (unsigned long long)na;
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tr[4] = smid;
@@ -602,6 +629,15 @@ void* kernel_for(int bn) {
     default: return kernel_ptr<256>();
   }
 }
+int kl_for(int bn) {
+  switch (bn) {
+    case 16: return quick::Cfg<16>::KL;
+    case 32: return quick::Cfg<32>::KL;
+    case 64: return quick::Cfg<64>::KL;
+    case 128: return quick::Cfg<128>::KL;
+    default: return quick::Cfg<256>::KL;
+  }
+}
 int smem_for(int bn) {
   switch (bn) {
     case 16: return quick::Cfg<16>::SMEM_BYTES;
@@ -680,7 +716,7 @@ int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <=
 //    residency is queried, not computed) and every CTA keeps >= 4 stages of K.
 Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
   (void)G;
-  const int KT = K / quick::kStageK;
+  const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
   const int tiles = (N / quick::kTileRows) * ((M + tn - 1) / tn);
   int S = 1;
@@ -689,7 +725,7 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
   } else {
     const int per_sm = (quick::kDCol + tn <= 256) ? 2 : 1;
     const int cap = per_sm * sm_count();
-    for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= KT / 4; ++s2) {
+    for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= NA / 2; ++s2) {
       if (tiles * s2 > cap) break;
       if (tiles > max_resident(tn, s2)) continue;
       S = s2;
@@ -775,20 +811,23 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
     return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
-  const int KT = K / quick::kStageK;
-  if (split_k < 0 || split_k > quick::kMaxSplit || split_k > KT) return QUICK_ERR_UNSUPPORTED;
+  const int NA = (K + quick::kKA - 1) / quick::kKA;
+  if (split_k < 0 || split_k > quick::kMaxSplit || split_k > NA) return QUICK_ERR_UNSUPPORTED;
 
   const Plan plan = choose_plan(M, N, K, G, tile_n, split_k);
   const int tn = plan.tile_n, s = plan.split;
 
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return cuda_fail(cudaErrorInitializationError);
+  // X viewed as [K/64][M][64] (dims innermost first: k within a 64-chunk, token, k-chunk): one
+  // 3-D box {64, tile_n, KL/64} lands as KL/64 SWIZZLE_128B [tile_n][64] sub-tiles.
   CUtensorMap tmap;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
-  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-  cuuint32_t box[2] = {(cuuint32_t)quick::kStageK, (cuuint32_t)tn};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(X), dims, strides,
+  const int kl = kl_for(tn);
+  cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)tn, (cuuint32_t)(kl / 64)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(X), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);

@@ -19,7 +19,7 @@ lib = quick.raw_library()
 lib.quick_debug_set_trace.argtypes = [ctypes.c_void_p]
 p = synth.make_problem(0, M, N, K, G)
 blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).cuda()
-copies = [blob.clone() for _ in range(max(2, int(3e8 // blob.numel())))]
+copies = [blob.clone() for _ in range(max(4, int(3e8 // blob.numel())))]
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((M, N), device="cuda", dtype=torch.float16)
 tr = torch.zeros(16 * STRIDE, dtype=torch.int64, device="cuda")
