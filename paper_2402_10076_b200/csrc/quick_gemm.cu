@@ -41,9 +41,8 @@ namespace quick {
 constexpr int kThreads = 320;     // 10 warps
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
-constexpr int kAStages = 2;       // depth of the TMEM A-operand ring
 constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
-constexpr int kDCol = kAStages * kAColsPerStage;  // accumulator columns start here (128)
+constexpr int kMaxAStages = 3;
 constexpr int kChunkBytes = kTileRows * 16;       // 32 k x 128 rows of int4 = one 2 KiB chunk
 constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-tile, group)
 constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable clusters)
@@ -56,6 +55,10 @@ constexpr int kTraceStride = 8 + 7 * kTraceStages;
 // costs ~150 SM cycles on B200 (measured with tools/trace_gemm.py).
 template <int BN>
 struct Cfg {
+  // TMEM: A ring (ASTAGES x 64 columns) then the fp32 accumulator (BN columns); 3 A stages fit
+  // in a 256-column allocation up to BN = 64 (2 CTAs per SM), 2 above
+  static constexpr int ASTAGES = BN <= 64 ? 3 : 2;
+  static constexpr int DCOL = ASTAGES * kAColsPerStage;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   static constexpr int STAGES = BN <= 16 ? 3 : BN <= 32 ? 3 : BN <= 64 ? 4 : 2;
@@ -67,11 +70,11 @@ struct Cfg {
   static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
   static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
   static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
-  // barriers: full[STAGES], empty[STAGES], afull[kAStages], aempty[kAStages], dfull
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * kAStages + 1;
+  // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 1;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = (kDCol + BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (DCOL + BN <= 256) ? 256 : 512;
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
   static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
@@ -165,6 +168,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES;
   constexpr int APL = C::APL;
+  constexpr int kAStages = C::ASTAGES;
+  constexpr int kDCol = C::DCOL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -327,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
     const uint8_t* wrow = smem + C::W_OFF + h * 2 * kChunkBytes + r * 16;
-    const bool tw = (q == 0 && lane == 0);   // this warp's lane 0 stamps the trace
+    const bool tw = (warp == 4 && lane == 0);   // one dequant warp stamps the trace
     uint32_t a_regs[32];
     // pipeline position of the A stage being loaded
     int slot = 0, sub = 0;
@@ -373,21 +378,27 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         }
       }
     };
+    // The A stage is released to the MMA as soon as its TMEM store completes; dequantizing
+    // the next stage then overlaps the MMAs of this one (ring of kAStages A stages).
     if (na > 0) load_dequant(0);
+    int as = 0;
+    uint32_t aph = 0;
     for (int a = 0; a < na; ++a) {
-      const int as = a & (kAStages - 1);
-      const uint32_t aph = (uint32_t)(a / kAStages) & 1u;
       const bool valid = (k_begin + a * kKA + 64 * h) < k_end;
       ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
       if (tw) stamp(3, a);
       ptx::tc_fence_after();
       if (valid) ptx::tmem_st_32x32b_x32(tmem + tlane + as * kAColsPerStage + h * 32, a_regs);
-      if (a + 1 < na) load_dequant(a + 1);   // overlaps the TMEM store above
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
       if (tw) stamp(4, a);
+      if (a + 1 < na) load_dequant(a + 1);
+      if (++as == kAStages) {
+        as = 0;
+        aph ^= 1u;
+      }
     }
     // ------------------------------------------------------------------ epilogue part 1
     constexpr int kColsPerWarp = BN / 2;
@@ -629,6 +640,15 @@ void* kernel_for(int bn) {
     default: return kernel_ptr<256>();
   }
 }
+int tmem_cols_for(int bn) {
+  switch (bn) {
+    case 16: return quick::Cfg<16>::TMEM_COLS;
+    case 32: return quick::Cfg<32>::TMEM_COLS;
+    case 64: return quick::Cfg<64>::TMEM_COLS;
+    case 128: return quick::Cfg<128>::TMEM_COLS;
+    default: return quick::Cfg<256>::TMEM_COLS;
+  }
+}
 int kl_for(int bn) {
   switch (bn) {
     case 16: return quick::Cfg<16>::KL;
@@ -723,7 +743,7 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
   if (force_split > 0) {
     S = force_split;
   } else {
-    const int per_sm = (quick::kDCol + tn <= 256) ? 2 : 1;
+    const int per_sm = 512 / tmem_cols_for(tn);
     const int cap = per_sm * sm_count();
     for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= NA / 2; ++s2) {
       if (tiles * s2 > cap) break;

@@ -14,9 +14,10 @@ from paper_2402_10076_b200 import quick  # noqa: E402
 
 OUT = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "tune.jsonl")
 shapes = [(4096, 4096), (13824, 5120), (5120, 13824), (28672, 8192), (8192, 28672)]
-if len(sys.argv) > 1 and sys.argv[1] == "quick":
-    shapes = [(4096, 4096)]
 Ms = [1, 4, 16, 32, 64, 128, 256, 512, 1024]
+if len(sys.argv) > 1 and sys.argv[1] == "quick":
+    shapes = [(4096, 4096), (28672, 8192)]
+    Ms = [1, 16, 64, 128, 256, 1024]
 G = 128
 dev = torch.device("cuda:0")
 stream = torch.cuda.Stream()
