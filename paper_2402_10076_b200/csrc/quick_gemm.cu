@@ -38,11 +38,10 @@
 
 namespace quick {
 
-constexpr int kThreads = 320;     // 10 warps
+constexpr int kThreads = 192;     // 6 warps: producer, MMA, 4 dequantizers (one per TMEM lane quarter)
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
 constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
-constexpr int kMaxAStages = 3;
 constexpr int kChunkBytes = kTileRows * 16;       // 32 k x 128 rows of int4 = one 2 KiB chunk
 constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-tile, group)
 constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable clusters)
@@ -159,7 +158,7 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
 }
 
-template <int BN>
+template <int BN, bool TRACE>
 __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const uint8_t* __restrict__ packed, void* __restrict__ Y, int M, int N,
@@ -205,10 +204,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
-      ptx::mbar_init(bar_empty + 8 * s, 8 + 1);  // 8 dequant warps + 1 MMA commit
+      ptx::mbar_init(bar_empty + 8 * s, 4 * 32 + 1);  // every dequant thread + 1 MMA commit
     }
     for (int a = 0; a < kAStages; ++a) {
-      ptx::mbar_init(bar_afull + 8 * a, 8);      // all 8 dequant warps write each A stage
+      ptx::mbar_init(bar_afull + 8 * a, 4 * 32);      // every dequant thread
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
     ptx::mbar_init(bar_dfull, 1);
@@ -220,14 +219,14 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  // debug tracing (tools/trace_gemm.py; null in production): clock64 stamps per stage
+  // debug tracing (TRACE instantiation only, tools/trace_gemm.py): clock64 stamps per stage
   unsigned long long* tr = nullptr;
-  if (trace != nullptr && blockIdx.z == 0 && blockIdx.y < 2)
+  if (TRACE && blockIdx.z == 0 && blockIdx.y < 2)
     tr = trace + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * kTraceStride;
   auto stamp = [&](int ev, int i) {
-    if (tr != nullptr && i < kTraceStages) tr[8 + ev * kTraceStages + i] = clock64();
+    if (TRACE && tr != nullptr && i < kTraceStages) tr[8 + ev * kTraceStages + i] = clock64();
   };
-  if (tr != nullptr && threadIdx.x == 0) tr[0] = clock64();
+  if (TRACE && tr != nullptr && threadIdx.x == 0) tr[0] = clock64();
   // let the next kernel in the stream launch its prologue early (PDL); it still waits for
   // this grid's completion before touching anything this grid writes
   ptx::griddep_launch_dependents();
@@ -286,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     int slot = 0, sub = 0, as = 0;
     uint32_t aph = 0;
     for (int a = 0; a < na; ++a) {
-      // A stage written by all 8 dequant warps; they waited on `full`, which also covers the
+      // A stage written by all 4 dequant warps; they waited on `full`, which also covers the
       // X tile of this load stage, so one wait orders both operands
       ptx::mbar_wait(bar_afull + 8 * as, aph);
       if (lane == 0) stamp(5, a);
@@ -322,53 +321,78 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     __syncwarp();
   } else {
     // ------------------------------------------------------------------ dequantizers
-    // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access) and k-half h of
-    // every 128-k A stage: per stage a thread (one TMEM lane = one weight row) loads 2 x 16 B
-    // = 64 codes, dequantizes them and writes 32 TMEM columns with one tcgen05.st.  The warp
-    // is software-pipelined: the tcgen05.st of stage a completes while it loads and
-    // dequantizes stage a + 1.
+    // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access); each of its
+    // threads (one TMEM lane = one weight row) dequantizes all 128 k of every A stage: 4 x
+    // LDS.128 = 128 codes -> 64 fp16x2 registers -> two tcgen05.st.32x32b.x32.  The group
+    // constants (s, 1024 + z, -(64 + z)) are rebuilt only when the group changes (G >= 128),
+    // or per 32-k chunk for G in {32, 64}.  Every thread arrives on the barriers itself (no
+    // warp-level election or divergence in the steady state).
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int h = (warp - 2) >> 2;       // k-half of each A stage handled by this warp
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
-    const uint8_t* wrow = smem + C::W_OFF + h * 2 * kChunkBytes + r * 16;
-    const bool tw = (warp == 4 && lane == 0);   // one dequant warp stamps the trace
-    uint32_t a_regs[32];
-    // pipeline position of the A stage being loaded
-    int slot = 0, sub = 0;
-    uint32_t ph = 0;
-    auto load_dequant = [&](int a) {
-      const int kl0 = k_begin + (a - sub) * kKA;          // first k of this load stage
-      const int ka = k_begin + a * kKA + 64 * h;          // first k of this warp's half
-      if (sub == 0 || a == 0) ptx::mbar_wait(bar_full + 8 * slot, ph);
+    const uint8_t* wrow = smem + C::W_OFF + r * 16;
+    const uint8_t* mrow = smem + C::M_OFF + r * 2;           // scale of row r in a meta block
+    const uint8_t* zrow = smem + C::M_OFF + 256 + (r >> 1);  // zero byte of row r
+    const uint32_t zsh = (uint32_t)(r & 1) * 4u;
+    const bool tw = TRACE && (warp == 2 && lane == 0);
+    const bool g_big = (G % kKA) == 0;    // a group spans whole A stages
+    uint32_t a_regs[64];
+    int slot = 0, sub = 0, as = 0;
+    uint32_t ph = 0, aph = 0;
+    int g_prev = -1;
+    DequantConsts cst = make_consts(0, 0);
+    for (int a = 0; a < na; ++a) {
+      const int ka = k_begin + a * kKA;
+      if (sub == 0) ptx::mbar_wait(bar_full + 8 * slot, ph);
       if (tw) stamp(2, a);
-      if (ka < k_end) {
-        const int g0 = group_of(kl0);
-        const uint8_t* meta = smem + C::M_OFF + slot * C::M_BYTES;
-        const uint8_t* meta0 = meta + (group_of(ka) - g0) * kMetaBytes;
-        const uint8_t* meta1 = meta + (group_of(ka + 32) - g0) * kMetaBytes;
-        const uint32_t s0 = reinterpret_cast<const uint16_t*>(meta0)[r];
-        const uint32_t z0 = meta0[256 + (r >> 1)];
-        const uint32_t s1 = reinterpret_cast<const uint16_t*>(meta1)[r];
-        const uint32_t z1 = meta1[256 + (r >> 1)];
-        const uint8_t* wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
-        const uint4 w0 = *reinterpret_cast<const uint4*>(wp);
-        const uint4 w1 = *reinterpret_cast<const uint4*>(wp + kChunkBytes);
-        __syncwarp();
-        if ((sub == APL - 1 || a == na - 1) && lane == 0) ptx::mbar_arrive(bar_empty + 8 * slot);
-        const DequantConsts c0 = make_consts(s0, (z0 >> ((r & 1) * 4)) & 0xFu);
-        const DequantConsts c1 = make_consts(s1, (z1 >> ((r & 1) * 4)) & 0xFu);
-        dequant_word(w0.x, c0, a_regs + 0);
-        dequant_word(w0.y, c0, a_regs + 4);
-        dequant_word(w0.z, c0, a_regs + 8);
-        dequant_word(w0.w, c0, a_regs + 12);
-        dequant_word(w1.x, c1, a_regs + 16);
-        dequant_word(w1.y, c1, a_regs + 20);
-        dequant_word(w1.z, c1, a_regs + 24);
-        dequant_word(w1.w, c1, a_regs + 28);
+      const int kl0 = ka - sub * kKA;     // first k of this load stage
+      const int g0 = group_of(kl0);
+      const uint8_t* wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
+      const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
+      const bool full_stage = (ka + kKA) <= k_end;
+      uint4 w[4];
+      w[0] = *reinterpret_cast<const uint4*>(wp);
+      w[1] = *reinterpret_cast<const uint4*>(wp + kChunkBytes);
+      if (full_stage) {
+        w[2] = *reinterpret_cast<const uint4*>(wp + 2 * kChunkBytes);
+        w[3] = *reinterpret_cast<const uint4*>(wp + 3 * kChunkBytes);
       } else {
-        __syncwarp();
-        if ((sub == APL - 1 || a == na - 1) && lane == 0) ptx::mbar_arrive(bar_empty + 8 * slot);
+        w[2] = make_uint4(0, 0, 0, 0);
+        w[3] = w[2];
+      }
+      if (g_big) {
+        const int g = group_of(ka);
+        if (g != g_prev) {
+          const uint32_t mo = moff + (uint32_t)(g - g0) * kMetaBytes;
+          cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo), (zrow[mo] >> zsh) & 0xFu);
+          g_prev = g;
+        }
+      }
+      const bool last_of_load = (sub == APL - 1) || (a == na - 1);
+      // (all loads of this stage are issued above; the arrive orders them before the refill)
+      if (last_of_load) ptx::mbar_arrive(bar_empty + 8 * slot);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (!g_big) {
+          const uint32_t mo = moff + (uint32_t)(group_of(ka + 32 * c) - g0) * kMetaBytes;
+          cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo), (zrow[mo] >> zsh) & 0xFu);
+        }
+        dequant_word(w[c].x, cst, a_regs + 16 * c + 0);
+        dequant_word(w[c].y, cst, a_regs + 16 * c + 4);
+        dequant_word(w[c].z, cst, a_regs + 16 * c + 8);
+        dequant_word(w[c].w, cst, a_regs + 16 * c + 12);
+      }
+      ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+      if (tw) stamp(3, a);
+      ptx::tc_fence_after();
+      ptx::tmem_st_32x32b_x64(tmem + tlane + as * kAColsPerStage, a_regs);
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(bar_afull + 8 * as);
+      if (tw) stamp(4, a);
+      if (++as == kAStages) {
+        as = 0;
+        aph ^= 1u;
       }
       if (++sub == APL || a == na - 1) {
         sub = 0;
@@ -377,44 +401,21 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
           ph ^= 1u;
         }
       }
-    };
-    // The A stage is released to the MMA as soon as its TMEM store completes; dequantizing
-    // the next stage then overlaps the MMAs of this one (ring of kAStages A stages).
-    if (na > 0) load_dequant(0);
-    int as = 0;
-    uint32_t aph = 0;
-    for (int a = 0; a < na; ++a) {
-      const bool valid = (k_begin + a * kKA + 64 * h) < k_end;
-      ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
-      if (tw) stamp(3, a);
-      ptx::tc_fence_after();
-      if (valid) ptx::tmem_st_32x32b_x32(tmem + tlane + as * kAColsPerStage + h * 32, a_regs);
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_afull + 8 * as);
-      if (tw) stamp(4, a);
-      if (a + 1 < na) load_dequant(a + 1);
-      if (++as == kAStages) {
-        as = 0;
-        aph ^= 1u;
-      }
     }
     // ------------------------------------------------------------------ epilogue part 1
-    constexpr int kColsPerWarp = BN / 2;
-    const int j0 = h * kColsPerWarp;
     const int n = t * kTileRows + r;
     if (na > 0) {
       ptx::mbar_wait(bar_dfull, 0);
       ptx::tc_fence_after();
     }
-    if (tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
+    if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
     float* part = reinterpret_cast<float*>(smem);  // [BN][128] fp32 (split-K only)
+    const int jmax = S == 1 ? min(BN, M - m0) : BN;   // columns (tokens) worth reading
 #pragma unroll 1
-    for (int jc = 0; jc < kColsPerWarp; jc += 8) {
+    for (int jc = 0; jc < jmax; jc += 8) {
       uint32_t v[8];
       if (na > 0) {
-        ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + j0 + jc, v);
+        ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + jc, v);
         ptx::tmem_wait_ld();
       } else {
 #pragma unroll
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       if (S == 1) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int m = m0 + j0 + jc + i;
+          const int m = m0 + jc + i;
           if (m < M) {
             const float f = __uint_as_float(v[i]);
             if (out_fp32)
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) part[(j0 + jc + i) * kTileRows + r] = __uint_as_float(v[i]);
+        for (int i = 0; i < 8; ++i) part[(jc + i) * kTileRows + r] = __uint_as_float(v[i]);
       }
     }
   }
@@ -448,10 +449,11 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
     const int eb = (int)(((int)my * E4) / S) * 4;
     const int ee = (int)((((int)my + 1) * E4) / S) * 4;
+    const int e_lim = min(ee, max(0, (M - m0)) * kTileRows);   // skip padded tokens
     uint32_t peer[kMaxSplit];
 #pragma unroll
     for (int p = 0; p < kMaxSplit; ++p) peer[p] = ptx::mapa(sbase, (uint32_t)(p < S ? p : 0));
-    for (int e = eb + (int)threadIdx.x * 4; e < ee; e += kThreads * 4) {
+    for (int e = eb + (int)threadIdx.x * 4; e < e_lim; e += kThreads * 4) {
       float4 v[kMaxSplit];
 #pragma unroll
       for (int p = 0; p < kMaxSplit; ++p)
@@ -468,18 +470,16 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
       const int m = m0 + j;
-      if (m < M) {
-        const size_t o = (size_t)m * ldy + (size_t)t * kTileRows + rr;
-        if (out_fp32) {
-          *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + o) = acc;
-        } else {
-          __half2 lo = __floats2half2_rn(acc.x, acc.y);
-          __half2 hi = __floats2half2_rn(acc.z, acc.w);
-          uint2 pk;
-          pk.x = *reinterpret_cast<uint32_t*>(&lo);
-          pk.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(Y) + o) = pk;
-        }
+      const size_t o = (size_t)m * ldy + (size_t)t * kTileRows + rr;
+      if (out_fp32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + o) = acc;
+      } else {
+        __half2 lo = __floats2half2_rn(acc.x, acc.y);
+        __half2 hi = __floats2half2_rn(acc.z, acc.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(Y) + o) = pk;
       }
     }
     ptx::cluster_sync();   // peers may still be reading our partials
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (tr != nullptr && threadIdx.x == 0) {
+  if (TRACE && tr != nullptr && threadIdx.x == 0) {
     tr[2] = clock64();
     tr[3] = (unsigned long long)na;
     uint32_t smid;
@@ -629,7 +629,7 @@ quick_status_t check_gemm_shape(int M, int N, int K, int G) {
 
 template <int BN>
 void* kernel_ptr() {
-  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN>);
+  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, false>);
 }
 void* kernel_for(int bn) {
   switch (bn) {
@@ -638,6 +638,19 @@ void* kernel_for(int bn) {
     case 64: return kernel_ptr<64>();
     case 128: return kernel_ptr<128>();
     default: return kernel_ptr<256>();
+  }
+}
+template <int BN>
+void* trace_kernel_ptr() {
+  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, true>);
+}
+void* trace_kernel_for(int bn) {
+  switch (bn) {
+    case 16: return trace_kernel_ptr<16>();
+    case 32: return trace_kernel_ptr<32>();
+    case 64: return trace_kernel_ptr<64>();
+    case 128: return trace_kernel_ptr<128>();
+    default: return trace_kernel_ptr<256>();
   }
 }
 int tmem_cols_for(int bn) {
@@ -677,6 +690,9 @@ cudaError_t configure_kernel(int bn) {
   if (done[dev][ti]) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_for(bn));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(trace_kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_for(bn));
   if (e == cudaSuccess) done[dev][ti] = true;
   return e;
 }
@@ -788,8 +804,12 @@ quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, i
     while ((1 << g_shift) < G) ++g_shift;
   }
   const uint8_t* pk = static_cast<const uint8_t*>(packed);
-  e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN>, tmap, pk, Y, M, N, K, G, g_shift,
-                         ldy, flags, g_trace);
+  if (g_trace != nullptr)
+    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, true>, tmap, pk, Y, M, N, K, G,
+                           g_shift, ldy, flags, g_trace);
+  else
+    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, false>, tmap, pk, Y, M, N, K, G,
+                           g_shift, ldy, flags, (unsigned long long*)nullptr);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
 }
