@@ -77,7 +77,8 @@ def test_onehot_rows_bit_exact(tile_n, split_k):
     np.testing.assert_array_equal(f16_bits(y), ref.view(np.uint16))
 
 
-@pytest.mark.parametrize("M,tile_n,split_k", [(9, 0, 0), (40, 32, 3), (130, 128, 2), (256, 256, 4), (5, 16, 8)])
+@pytest.mark.parametrize("M,tile_n,split_k", [(9, 0, 0), (40, 32, 3), (130, 128, 2), (256, 256, 4), (5, 16, 8),
+                                             (70, 64, 5), (20, 16, 1)])
 def test_integer_exact_regime_bit_exact(M, tile_n, split_k):
     p = synth.make_structured("intexact", 5, M=M, N=384, K=1024, G=128)
     y = run(p, tile_n=tile_n, split_k=split_k)
@@ -103,7 +104,7 @@ def test_tiny_config_all_paths():
     """BASELINE.json configs[0]: M=8, N=256, K=512, G=128."""
     p = synth.make_problem(0, M=8, N=256, K=512, G=128)
     for tile_n in (0, 16, 32, 64, 128, 256):
-        for split_k in (0, 1, 2, 4, 8):
+        for split_k in (0, 1, 2, 3, 4):   # K = 512 is 4 A stages of 128 k
             check_tol(p, run(p, tile_n=tile_n, split_k=split_k), (tile_n, split_k))
 
 
@@ -126,6 +127,7 @@ def test_group_sizes(G):
         pytest.skip("K not a multiple of G")
     check_tol(p, run(p))
     check_tol(p, run(p, split_k=3))
+    check_tol(p, run(p, tile_n=128))      # non-group-scaled path at every G
 
 
 @pytest.mark.parametrize("M", [1, 2, 4, 8, 16, 32, 64, 128, 256])
