@@ -127,6 +127,7 @@ def test_group_sizes(G):
         pytest.skip("K not a multiple of G")
     check_tol(p, run(p))
     check_tol(p, run(p, split_k=3))
+    check_tol(p, run(p, tile_n=128))
     check_tol(p, run(p, tile_n=128))      # non-group-scaled path at every G
 
 
