@@ -52,13 +52,11 @@ constexpr int kTraceStride = 8 + 7 * kTraceStages;
 // weights, one bulk copy of the groups' metadata, one 3-D TMA of the [KL/64][BN][64] X tile),
 // STAGES = depth of the load ring.  Few, large async copies per byte: each TMA/bulk issue
 // costs ~150 SM cycles on B200 (measured with tools/trace_gemm.py).
-template <int BN, bool GS>
+template <int BN>
 struct Cfg {
-  // TMEM: A ring (ASTAGES x 64 columns), then NDBUF fp32 accumulators of BN columns.  GS
-  // ("group-scaled"): one accumulator per quantization group, double
-  // buffered, scaled by s_g in fp32 after the MMA, so the dequantizers skip the HMUL2.
-  static constexpr int NDBUF = GS ? 2 : 1;
-  static constexpr int ASTAGES = (BN <= 64 && 3 * kAColsPerStage + NDBUF * BN <= 256) ? 3 : 2;
+  // TMEM: A ring (ASTAGES x 64 columns) then the fp32 accumulator (BN columns); 3 A stages fit
+  // in a 256-column allocation up to BN = 64 (2 CTAs per SM), 2 above
+  static constexpr int ASTAGES = BN <= 64 ? 3 : 2;
   static constexpr int DCOL = ASTAGES * kAColsPerStage;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
@@ -71,12 +69,11 @@ struct Cfg {
   static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
   static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
   static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
-  // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull,
-  //           gfull[2], gempty[2]
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 1 + 4;
+  // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 1;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = (DCOL + NDBUF * BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (DCOL + BN <= 256) ? 256 : 512;
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
   static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
@@ -84,7 +81,6 @@ struct Cfg {
   static constexpr int SMEM_BYTES = (USED + 1024 > MIN_SMEM ? USED + 1024 : MIN_SMEM);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
   static_assert(KL % kKA == 0, "load stage = whole A stages");
-  static_assert(!GS || BN <= 64, "group-scaled mode keeps BN fp32 accumulators in registers");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // split-K partial tile [BN][128] fp32 reuses the pipeline buffers once the mainloop is done
   static_assert(BN * kTileRows * 4 <= BAR_OFF, "split-K partial must fit in the pipeline smem");
@@ -145,22 +141,6 @@ __device__ __forceinline__ void dequant_word(uint32_t w, const DequantConsts& c,
   out[3] = hmul2_rn(hfma2_rn(hi1, kInv16, c.zhi), c.s2);
 }
 
-// GS mode: the same extraction without the scale multiply -> exact (q - z) in fp16
-__device__ __forceinline__ void dequant_word_noscale(uint32_t w, const DequantConsts& c,
-                                                     uint32_t* out) {
-  constexpr uint32_t kMagic = 0x64006400u;
-  constexpr uint32_t kInv16 = 0x2C002C00u;
-  const uint32_t lo0 = ptx::lop3<0xEA>(w, 0x000F000Fu, kMagic);
-  const uint32_t hi0 = ptx::lop3<0xEA>(w, 0x00F000F0u, kMagic);
-  const uint32_t w8 = w >> 8;
-  const uint32_t lo1 = ptx::lop3<0xEA>(w8, 0x000F000Fu, kMagic);
-  const uint32_t hi1 = ptx::lop3<0xEA>(w8, 0x00F000F0u, kMagic);
-  out[0] = hsub2_rn(lo0, c.zlo);
-  out[1] = hfma2_rn(hi0, kInv16, c.zhi);
-  out[2] = hsub2_rn(lo1, c.zlo);
-  out[3] = hfma2_rn(hi1, kInv16, c.zhi);
-}
-
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), version 1
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   uint64_t d = 0;
@@ -178,13 +158,13 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
 }
 
-template <int BN, bool GS, bool TRACE>
-__global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
+template <int BN, bool TRACE>
+__global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const uint8_t* __restrict__ packed, void* __restrict__ Y, int M, int N,
                           int K, int G, int g_shift, int ldy, int flags,
                           unsigned long long* __restrict__ trace) {
-  using C = Cfg<BN, GS>;
+  using C = Cfg<BN>;
   constexpr int STAGES = C::STAGES;
   constexpr int APL = C::APL;
   constexpr int kAStages = C::ASTAGES;
@@ -219,8 +199,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
   const uint32_t bar_afull = bar_empty + 8 * STAGES;
   const uint32_t bar_aempty = bar_afull + 8 * kAStages;
   const uint32_t bar_dfull = bar_aempty + 8 * kAStages;
-  const uint32_t bar_gfull = bar_dfull + 8;       // GS: group accumulator b complete
-  const uint32_t bar_gempty = bar_gfull + 16;     // GS: group accumulator b read out
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::HOLD_OFF);
 
   if (threadIdx.x == 0) {
@@ -233,10 +211,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
     ptx::mbar_init(bar_dfull, 1);
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(bar_gfull + 8 * b, 1);
-      ptx::mbar_init(bar_gempty + 8 * b, 4 * 32);
-    }
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
@@ -310,45 +284,27 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
     int slot = 0, sub = 0, as = 0;
     uint32_t aph = 0;
-    int gi = -1, g_cur = -1;   // GS: local group counter / current group
     for (int a = 0; a < na; ++a) {
-      const int ka = k_begin + a * kKA;
-      bool first_of_group = false, last_of_group = false;
-      if (GS) {
-        const int g = group_of(ka);
-        first_of_group = (g != g_cur);
-        if (first_of_group) {
-          ++gi;
-          g_cur = g;
-          // accumulator (gi & 1) must have been read out for group gi - 2
-          if (gi >= 2) ptx::mbar_wait(bar_gempty + 8 * (gi & 1), (uint32_t)(((gi >> 1) + 1) & 1));
-        }
-        last_of_group = (a == na - 1) || (group_of(ka + kKA) != g);
-      }
       // A stage written by all 4 dequant warps; they waited on `full`, which also covers the
       // X tile of this load stage, so one wait orders both operands
       ptx::mbar_wait(bar_afull + 8 * as, aph);
       if (lane == 0) stamp(5, a);
       ptx::tc_fence_after();
-      const int kv = min(kKA, k_end - ka);   // 128, or 64 at the end of K
+      const int kv = min(kKA, k_end - (k_begin + a * kKA));   // 128, or 64 at the end of K
       if (ptx::elect_one()) {
         const uint32_t a_col = tmem + as * kAColsPerStage;
-        const uint32_t d_col = tmem + kDCol + (GS ? (uint32_t)((gi & 1) * BN) : 0u);
         // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
         const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES + sub * 2 * C::X_SUB) >> 4);
 #pragma unroll
         for (int kk = 0; kk < kKA / 16; ++kk) {
-          if (kk * 16 < kv) {
-            const bool acc = GS ? !(first_of_group && kk == 0) : ((a | kk) != 0);
-            ptx::mma_f16_ts(d_col, a_col + kk * 8,
+          if (kk * 16 < kv)
+            ptx::mma_f16_ts(tmem + kDCol, a_col + kk * 8,
                             dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
-                            acc ? 1u : 0u);
-          }
+                            (a | kk) != 0 ? 1u : 0u);
         }
         ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
         if (sub == APL - 1 || a == na - 1)
           ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage consumed
-        if (GS && last_of_group) ptx::mma_commit(bar_gfull + 8 * (gi & 1));
       }
       __syncwarp();
       if (lane == 0) stamp(6, a);
@@ -385,33 +341,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
     uint32_t ph = 0, aph = 0;
     int g_prev = -1;
     DequantConsts cst = make_consts(0, 0);
-    // GS: fp32 output accumulators of this row for the valid tokens, the local index of the
-    // group whose TMEM accumulator is waiting to be scaled, and that group's scale
-    const int jmax = (S == 1) ? min(BN, M - m0) : BN;
-    float acc[GS ? BN : 1];
-#pragma unroll
-    for (int j = 0; j < (GS ? BN : 1); ++j) acc[j] = 0.f;
-    int gi = -1, pend_gi = -1;
-    float s_cur = 0.f, pend_s = 0.f;
-    auto scale_group = [&](int g_idx, float sc) {
-      // acc[j] += s_g * D_g[row][j]: the group's exact sum of (q - z) x, scaled in fp32
-      ptx::mbar_wait(bar_gfull + 8 * (g_idx & 1), (uint32_t)((g_idx >> 1) & 1));
-      ptx::tc_fence_after();
-      const uint32_t dcol = tmem + tlane + kDCol + (uint32_t)((g_idx & 1) * BN);
-#pragma unroll
-      for (int jc = 0; jc < (GS ? BN : 8); jc += 8) {
-        if (jc < jmax) {
-          uint32_t v[8];
-          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (GS) acc[jc + i] = fmaf(sc, __uint_as_float(v[i]), acc[jc + i]);
-        }
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(bar_gempty + 8 * (g_idx & 1));
-    };
     for (int a = 0; a < na; ++a) {
       const int ka = k_begin + a * kKA;
       if (sub == 0) ptx::mbar_wait(bar_full + 8 * slot, ph);
@@ -435,12 +364,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
         const int g = group_of(ka);
         if (g != g_prev) {
           const uint32_t mo = moff + (uint32_t)(g - g0) * kMetaBytes;
-          const uint32_t sb = *reinterpret_cast<const uint16_t*>(mrow + mo);
-          cst = make_consts(sb, (zrow[mo] >> zsh) & 0xFu);
-          if (GS) {
-            s_cur = __half2float(__ushort_as_half((unsigned short)sb));
-            ++gi;
-          }
+          cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo), (zrow[mo] >> zsh) & 0xFu);
           g_prev = g;
         }
       }
@@ -453,17 +377,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
           const uint32_t mo = moff + (uint32_t)(group_of(ka + 32 * c) - g0) * kMetaBytes;
           cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo), (zrow[mo] >> zsh) & 0xFu);
         }
-        if (GS) {
-          dequant_word_noscale(w[c].x, cst, a_regs + 16 * c + 0);
-          dequant_word_noscale(w[c].y, cst, a_regs + 16 * c + 4);
-          dequant_word_noscale(w[c].z, cst, a_regs + 16 * c + 8);
-          dequant_word_noscale(w[c].w, cst, a_regs + 16 * c + 12);
-        } else {
-          dequant_word(w[c].x, cst, a_regs + 16 * c + 0);
-          dequant_word(w[c].y, cst, a_regs + 16 * c + 4);
-          dequant_word(w[c].z, cst, a_regs + 16 * c + 8);
-          dequant_word(w[c].w, cst, a_regs + 16 * c + 12);
-        }
+        dequant_word(w[c].x, cst, a_regs + 16 * c + 0);
+        dequant_word(w[c].y, cst, a_regs + 16 * c + 4);
+        dequant_word(w[c].z, cst, a_regs + 16 * c + 8);
+        dequant_word(w[c].w, cst, a_regs + 16 * c + 12);
       }
       ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
       if (tw) stamp(3, a);
@@ -473,17 +390,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
       ptx::tc_fence_before();
       ptx::mbar_arrive(bar_afull + 8 * as);
       if (tw) stamp(4, a);
-      if (GS) {
-        // scale the previous group one stage late, when its MMAs have long completed
-        if (pend_gi >= 0) {
-          scale_group(pend_gi, pend_s);
-          pend_gi = -1;
-        }
-        if (a == na - 1 || group_of(ka + kKA) != g_prev) {
-          pend_gi = gi;
-          pend_s = s_cur;
-        }
-      }
       if (++as == kAStages) {
         as = 0;
         aph ^= 1u;
@@ -498,31 +404,15 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, GS>::MAX_CTAS_PER_SM)
     }
     // ------------------------------------------------------------------ epilogue part 1
     const int n = t * kTileRows + r;
-    if (GS && pend_gi >= 0) scale_group(pend_gi, pend_s);
     if (na > 0) {
       ptx::mbar_wait(bar_dfull, 0);
       ptx::tc_fence_after();
     }
     if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
     float* part = reinterpret_cast<float*>(smem);  // [BN][128] fp32 (split-K only)
-    if (GS) {
-#pragma unroll
-      for (int j = 0; j < (GS ? BN : 1); ++j) {
-        if (j < jmax) {
-          if (S == 1) {
-            const size_t o = (size_t)(m0 + j) * ldy + n;
-            if (out_fp32)
-              reinterpret_cast<float*>(Y)[o] = acc[j];
-            else
-              reinterpret_cast<__half*>(Y)[o] = __float2half_rn(acc[j]);
-          } else {
-            part[j * kTileRows + r] = acc[j];
-          }
-        }
-      }
-    }
+    const int jmax = S == 1 ? min(BN, M - m0) : BN;   // columns (tokens) worth reading
 #pragma unroll 1
-    for (int jc = 0; jc < (GS ? 0 : jmax); jc += 8) {
+    for (int jc = 0; jc < jmax; jc += 8) {
       uint32_t v[8];
       if (na > 0) {
         ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + jc, v);
@@ -737,79 +627,99 @@ quick_status_t check_gemm_shape(int M, int N, int K, int G) {
   return QUICK_OK;
 }
 
-// tile widths with a group-scaled (GS) variant
-inline bool gs_capable(int bn) { return bn <= 64; }
-
-template <int BN, bool GS, bool TRACE>
+template <int BN>
 void* kernel_ptr() {
-  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, GS, TRACE>);
+  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, false>);
 }
-template <bool TRACE>
-void* kernel_for_t(int bn, bool gs) {
+void* kernel_for(int bn) {
   switch (bn) {
-    case 16: return gs ? kernel_ptr<16, true, TRACE>() : kernel_ptr<16, false, TRACE>();
-    case 32: return gs ? kernel_ptr<32, true, TRACE>() : kernel_ptr<32, false, TRACE>();
-    case 64: return gs ? kernel_ptr<64, true, TRACE>() : kernel_ptr<64, false, TRACE>();
-    case 128: return kernel_ptr<128, false, TRACE>();
-    default: return kernel_ptr<256, false, TRACE>();
+    case 16: return kernel_ptr<16>();
+    case 32: return kernel_ptr<32>();
+    case 64: return kernel_ptr<64>();
+    case 128: return kernel_ptr<128>();
+    default: return kernel_ptr<256>();
   }
 }
-void* kernel_for(int bn, bool gs = false) { return kernel_for_t<false>(bn, gs); }
-void* trace_kernel_for(int bn, bool gs = false) { return kernel_for_t<true>(bn, gs); }
-#define QUICK_CFG_FIELD(FN, FIELD)                                           \
-  int FN(int bn, bool gs = false) {                                          \
-    switch (bn) {                                                            \
-      case 16: return gs ? quick::Cfg<16, true>::FIELD : quick::Cfg<16, false>::FIELD; \
-      case 32: return gs ? quick::Cfg<32, true>::FIELD : quick::Cfg<32, false>::FIELD; \
-      case 64: return gs ? quick::Cfg<64, true>::FIELD : quick::Cfg<64, false>::FIELD; \
-      case 128: return quick::Cfg<128, false>::FIELD;                       \
-      default: return quick::Cfg<256, false>::FIELD;                        \
-    }                                                                        \
+template <int BN>
+void* trace_kernel_ptr() {
+  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, true>);
+}
+void* trace_kernel_for(int bn) {
+  switch (bn) {
+    case 16: return trace_kernel_ptr<16>();
+    case 32: return trace_kernel_ptr<32>();
+    case 64: return trace_kernel_ptr<64>();
+    case 128: return trace_kernel_ptr<128>();
+    default: return trace_kernel_ptr<256>();
   }
-QUICK_CFG_FIELD(tmem_cols_for, TMEM_COLS)
-QUICK_CFG_FIELD(kl_for, KL)
-QUICK_CFG_FIELD(smem_for, SMEM_BYTES)
-#undef QUICK_CFG_FIELD
+}
+int tmem_cols_for(int bn) {
+  switch (bn) {
+    case 16: return quick::Cfg<16>::TMEM_COLS;
+    case 32: return quick::Cfg<32>::TMEM_COLS;
+    case 64: return quick::Cfg<64>::TMEM_COLS;
+    case 128: return quick::Cfg<128>::TMEM_COLS;
+    default: return quick::Cfg<256>::TMEM_COLS;
+  }
+}
+int kl_for(int bn) {
+  switch (bn) {
+    case 16: return quick::Cfg<16>::KL;
+    case 32: return quick::Cfg<32>::KL;
+    case 64: return quick::Cfg<64>::KL;
+    case 128: return quick::Cfg<128>::KL;
+    default: return quick::Cfg<256>::KL;
+  }
+}
+int smem_for(int bn) {
+  switch (bn) {
+    case 16: return quick::Cfg<16>::SMEM_BYTES;
+    case 32: return quick::Cfg<32>::SMEM_BYTES;
+    case 64: return quick::Cfg<64>::SMEM_BYTES;
+    case 128: return quick::Cfg<128>::SMEM_BYTES;
+    default: return quick::Cfg<256>::SMEM_BYTES;
+  }
+}
 
-// one-time per (device, tile, mode): opt into the dynamic shared memory the config needs
-cudaError_t configure_kernel(int bn, bool gs) {
+// one-time per (device, tile): opt into the dynamic shared memory the config needs
+cudaError_t configure_kernel(int bn) {
   static std::mutex mu;
-  static bool done[kMaxDev][5][2] = {};
+  static bool done[kMaxDev][5] = {};
   const int dev = current_device(), ti = tile_index(bn);
   std::lock_guard<std::mutex> lock(mu);
-  if (done[dev][ti][gs]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel_for(bn, gs),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(bn, gs));
+  if (done[dev][ti]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_for(bn));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(trace_kernel_for(bn, gs), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem_for(bn, gs));
-  if (e == cudaSuccess) done[dev][ti][gs] = true;
+    e = cudaFuncSetAttribute(trace_kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_for(bn));
+  if (e == cudaSuccess) done[dev][ti] = true;
   return e;
 }
 
 // How many clusters of S CTAs (or, for S == 1, CTAs) can be resident at once on this device.
 // Cluster placement is GPC-constrained, so this is not simply SMs * CTAs-per-SM / S.
-int max_resident(int bn, bool gs, int S) {
+int max_resident(int bn, int S) {
   static std::mutex mu;
-  static int cache[kMaxDev][5][2][quick::kMaxSplit + 1] = {};
+  static int cache[kMaxDev][5][quick::kMaxSplit + 1] = {};
   const int dev = current_device(), ti = tile_index(bn);
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (cache[dev][ti][gs][S]) return cache[dev][ti][gs][S];
+    if (cache[dev][ti][S]) return cache[dev][ti][S];
   }
   int n = 0;
-  if (configure_kernel(bn, gs) == cudaSuccess) {
+  if (configure_kernel(bn) == cudaSuccess) {
     if (S == 1) {
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(bn, gs), quick::kThreads,
-                                                        smem_for(bn, gs)) == cudaSuccess)
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(bn), quick::kThreads,
+                                                        smem_for(bn)) == cudaSuccess)
         n = per_sm * sm_count();
     } else {
       cudaLaunchConfig_t cfg;
       std::memset(&cfg, 0, sizeof(cfg));
       cfg.gridDim = dim3((unsigned)S, 1, 1);
       cfg.blockDim = dim3(quick::kThreads, 1, 1);
-      cfg.dynamicSmemBytes = smem_for(bn, gs);
+      cfg.dynamicSmemBytes = smem_for(bn);
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeClusterDimension;
       attr.val.clusterDim.x = (unsigned)S;
@@ -817,20 +727,19 @@ int max_resident(int bn, bool gs, int S) {
       attr.val.clusterDim.z = 1;
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&n, kernel_for(bn, gs), &cfg) != cudaSuccess) n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kernel_for(bn), &cfg) != cudaSuccess) n = 0;
     }
   }
   cudaGetLastError();  // occupancy queries must not leave a sticky error behind
   if (n <= 0) n = (S == 1 ? sm_count() : sm_count() / (2 * S));
   if (n <= 0) n = 1;
   std::lock_guard<std::mutex> lock(mu);
-  cache[dev][ti][gs][S] = n;
+  cache[dev][ti][S] = n;
   return n;
 }
 
 struct Plan {
   int tile_n, split, ctas;
-  bool gs;
 };
 
 int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
@@ -838,36 +747,34 @@ int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <=
 // Launch plan (tuned with tools/tune_plan.py on B200):
 //  - tokens per tile: the smallest MMA N covering M (weights are dequantized once per m-tile,
 //    so larger M uses the widest tile; M > 256 tiles the tokens by 256);
-//  - group-scaled mode (per-group TMEM accumulators, fp32 scale after the MMA) whenever the
-//    groups are whole 128-k A stages and the tile keeps its accumulators in registers;
 //  - split-K: the largest S <= 8 such that all tiles x S CTAs are resident in one wave (TMEM
 //    and shared memory allow 2 CTAs/SM up to tile 128, 1 above; clusters are GPC-placed, so
-//    residency is queried, not computed) and every CTA keeps >= 2 A stages of K.
+//    residency is queried, not computed) and every CTA keeps >= 4 stages of K.
 Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
+  (void)G;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
-  const bool gs = gs_capable(tn) && (G % quick::kKA == 0);
   const int tiles = (N / quick::kTileRows) * ((M + tn - 1) / tn);
   int S = 1;
   if (force_split > 0) {
     S = force_split;
   } else {
-    const int per_sm = 512 / tmem_cols_for(tn, gs);
+    const int per_sm = 512 / tmem_cols_for(tn);
     const int cap = per_sm * sm_count();
     for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= NA / 2; ++s2) {
       if (tiles * s2 > cap) break;
-      if (tiles > max_resident(tn, gs, s2)) continue;
+      if (tiles > max_resident(tn, s2)) continue;
       S = s2;
     }
   }
-  return Plan{tn, S, tiles * S, gs};
+  return Plan{tn, S, tiles * S};
 }
 
-template <int BN, bool GS>
+template <int BN>
 quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, int M, int N, int K,
                          int G, int ldy, int flags, int S, cudaStream_t stream) {
-  using C = quick::Cfg<BN, GS>;
-  cudaError_t e = configure_kernel(BN, GS);
+  using C = quick::Cfg<BN>;
+  cudaError_t e = configure_kernel(BN);
   if (e != cudaSuccess) return cuda_fail(e);
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
@@ -898,11 +805,11 @@ quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, i
   }
   const uint8_t* pk = static_cast<const uint8_t*>(packed);
   if (g_trace != nullptr)
-    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, GS, true>, tmap, pk, Y, M, N, K,
-                           G, g_shift, ldy, flags, g_trace);
+    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, true>, tmap, pk, Y, M, N, K, G,
+                           g_shift, ldy, flags, g_trace);
   else
-    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, GS, false>, tmap, pk, Y, M, N, K,
-                           G, g_shift, ldy, flags, (unsigned long long*)nullptr);
+    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, false>, tmap, pk, Y, M, N, K, G,
+                           g_shift, ldy, flags, (unsigned long long*)nullptr);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
 }
@@ -955,7 +862,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   // X viewed as [K/64][M][64] (dims innermost first: k within a 64-chunk, token, k-chunk): one
   // 3-D box {64, tile_n, KL/64} lands as KL/64 SWIZZLE_128B [tile_n][64] sub-tiles.
   CUtensorMap tmap;
-  const int kl = kl_for(tn, plan.gs);
+  const int kl = kl_for(tn);
   cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
   cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
   cuuint32_t box[3] = {64, (cuuint32_t)tn, (cuuint32_t)(kl / 64)};
@@ -966,19 +873,12 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (cr != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
 
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
-  const bool gs = plan.gs;
   switch (tn) {
-    case 16:
-      return gs ? launch_bn<16, true>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm)
-                : launch_bn<16, false>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    case 32:
-      return gs ? launch_bn<32, true>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm)
-                : launch_bn<32, false>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    case 64:
-      return gs ? launch_bn<64, true>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm)
-                : launch_bn<64, false>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    case 128: return launch_bn<128, false>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    default: return launch_bn<256, false>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 16: return launch_bn<16>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 32: return launch_bn<32>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 64: return launch_bn<64>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 128: return launch_bn<128>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    default: return launch_bn<256>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
   }
 }
 
