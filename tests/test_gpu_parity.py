@@ -128,7 +128,6 @@ def test_group_sizes(G):
     check_tol(p, run(p))
     check_tol(p, run(p, split_k=3))
     check_tol(p, run(p, tile_n=128))
-    check_tol(p, run(p, tile_n=128))      # non-group-scaled path at every G
 
 
 @pytest.mark.parametrize("M", [1, 2, 4, 8, 16, 32, 64, 128, 256])
