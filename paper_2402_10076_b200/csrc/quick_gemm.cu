@@ -38,7 +38,7 @@
 
 namespace quick {
 
-constexpr int kThreads = 192;     // 6 warps: producer, MMA, 4 dequantizers (one per TMEM lane quarter)
+constexpr int kThreads = 320;     // 10 warps: producer, MMA, 8 dequantizers (2 per TMEM lane quarter)
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
 constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
@@ -204,10 +204,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
-      ptx::mbar_init(bar_empty + 8 * s, 4 * 32 + 1);  // every dequant thread + 1 MMA commit
+      // every thread of the dequant warps reading this load stage (both parities when it holds
+      // two A stages, one parity otherwise) + 1 MMA commit
+      ptx::mbar_init(bar_empty + 8 * s, 4 * 32 * (APL >= 2 ? 2 : 1) + 1);
     }
     for (int a = 0; a < kAStages; ++a) {
-      ptx::mbar_init(bar_afull + 8 * a, 4 * 32);      // every dequant thread
+      ptx::mbar_init(bar_afull + 8 * a, 4 * 32);      // every thread of one parity group
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
     ptx::mbar_init(bar_dfull, 1);
@@ -321,13 +323,15 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     __syncwarp();
   } else {
     // ------------------------------------------------------------------ dequantizers
-    // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access); each of its
-    // threads (one TMEM lane = one weight row) dequantizes all 128 k of every A stage: 4 x
-    // LDS.128 = 128 codes -> 64 fp16x2 registers -> two tcgen05.st.32x32b.x32.  The group
-    // constants (s, 1024 + z, -(64 + z)) are rebuilt only when the group changes (G >= 128),
-    // or per 32-k chunk for G in {32, 64}.  Every thread arrives on the barriers itself (no
-    // warp-level election or divergence in the steady state).
+    // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access) and takes the
+    // A stages of parity p (two warps per quarter, so each SM sub-partition interleaves two
+    // independent dequant streams per CTA).  Per A stage a thread (one TMEM lane = one weight
+    // row) loads 4 x 16 B = 128 codes and writes 64 TMEM columns in two tcgen05.st.32x32b.x32;
+    // the second half is dequantized while the first store drains.  Group constants (s,
+    // 1024 + z, -(64 + z)) are rebuilt only when the group changes (G % 128 == 0), or per
+    // 32-k chunk otherwise.  Every thread arrives on the barriers itself.
     const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int p = (warp - 2) >> 2;       // parity of the A stages this warp dequantizes
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
     const uint8_t* wrow = smem + C::W_OFF + r * 16;
@@ -336,17 +340,17 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     const uint32_t zsh = (uint32_t)(r & 1) * 4u;
     const bool tw = TRACE && (warp == 2 && lane == 0);
     const bool g_big = (G % kKA) == 0;    // a group spans whole A stages
-    uint32_t a_regs[64];
-    int slot = 0, sub = 0, as = 0;
-    uint32_t ph = 0, aph = 0;
+    uint32_t a_regs[32];
     int g_prev = -1;
     DequantConsts cst = make_consts(0, 0);
-    for (int a = 0; a < na; ++a) {
+    for (int a = p; a < na; a += 2) {
       const int ka = k_begin + a * kKA;
-      if (sub == 0) ptx::mbar_wait(bar_full + 8 * slot, ph);
+      const int l = a / APL;               // load stage of this A stage
+      const int sub = a - l * APL;
+      const int slot = l % STAGES;
+      ptx::mbar_wait(bar_full + 8 * slot, (uint32_t)((l / STAGES) & 1));
       if (tw) stamp(2, a);
-      const int kl0 = ka - sub * kKA;     // first k of this load stage
-      const int g0 = group_of(kl0);
+      const int g0 = group_of(ka - sub * kKA);
       const uint8_t* wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
       const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
       const bool full_stage = (ka + kKA) <= k_end;
@@ -368,41 +372,57 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
           g_prev = g;
         }
       }
-      const bool last_of_load = (sub == APL - 1) || (a == na - 1);
-      // (all loads of this stage are issued above; the arrive orders them before the refill)
-      if (last_of_load) ptx::mbar_arrive(bar_empty + 8 * slot);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (!g_big) {
-          const uint32_t mo = moff + (uint32_t)(group_of(ka + 32 * c) - g0) * kMetaBytes;
-          cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo), (zrow[mo] >> zsh) & 0xFu);
-        }
-        dequant_word(w[c].x, cst, a_regs + 16 * c + 0);
-        dequant_word(w[c].y, cst, a_regs + 16 * c + 4);
-        dequant_word(w[c].z, cst, a_regs + 16 * c + 8);
-        dequant_word(w[c].w, cst, a_regs + 16 * c + 12);
+      DequantConsts cst1 = cst;
+      if (!g_big) {
+        const uint32_t mo0 = moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes;
+        const uint32_t mo1 = moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes;
+        cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo0), (zrow[mo0] >> zsh) & 0xFu);
+        cst1 = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo1), (zrow[mo1] >> zsh) & 0xFu);
       }
+      // this warp reads exactly one A stage of each load stage it touches
+      ptx::mbar_arrive(bar_empty + 8 * slot);
+      const int as = a % kAStages;
+      const uint32_t aph = (uint32_t)((a / kAStages) & 1);
+      dequant_word(w[0].x, cst, a_regs + 0);
+      dequant_word(w[0].y, cst, a_regs + 4);
+      dequant_word(w[0].z, cst, a_regs + 8);
+      dequant_word(w[0].w, cst, a_regs + 12);
+      dequant_word(w[1].x, cst1, a_regs + 16);
+      dequant_word(w[1].y, cst1, a_regs + 20);
+      dequant_word(w[1].z, cst1, a_regs + 24);
+      dequant_word(w[1].w, cst1, a_regs + 28);
       ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
       if (tw) stamp(3, a);
       ptx::tc_fence_after();
-      ptx::tmem_st_32x32b_x64(tmem + tlane + as * kAColsPerStage, a_regs);
+      const uint32_t acol = tmem + tlane + as * kAColsPerStage;
+      ptx::tmem_st_32x32b_x32(acol, a_regs);
+      if (full_stage) {
+        DequantConsts cst2 = cst, cst3 = cst;
+        if (!g_big) {
+          const uint32_t mo2 = moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes;
+          const uint32_t mo3 = moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes;
+          cst2 = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo2), (zrow[mo2] >> zsh) & 0xFu);
+          cst3 = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo3), (zrow[mo3] >> zsh) & 0xFu);
+        }
+        uint32_t b_regs[32];
+        dequant_word(w[2].x, cst2, b_regs + 0);
+        dequant_word(w[2].y, cst2, b_regs + 4);
+        dequant_word(w[2].z, cst2, b_regs + 8);
+        dequant_word(w[2].w, cst2, b_regs + 12);
+        dequant_word(w[3].x, cst3, b_regs + 16);
+        dequant_word(w[3].y, cst3, b_regs + 20);
+        dequant_word(w[3].z, cst3, b_regs + 24);
+        dequant_word(w[3].w, cst3, b_regs + 28);
+        ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+      }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(bar_afull + 8 * as);
       if (tw) stamp(4, a);
-      if (++as == kAStages) {
-        as = 0;
-        aph ^= 1u;
-      }
-      if (++sub == APL || a == na - 1) {
-        sub = 0;
-        if (++slot == STAGES) {
-          slot = 0;
-          ph ^= 1u;
-        }
-      }
     }
     // ------------------------------------------------------------------ epilogue part 1
+    constexpr int kColsPerWarp = BN / 2;
+    const int j0 = p * kColsPerWarp;     // this warp's half of the accumulator columns
     const int n = t * kTileRows + r;
     if (na > 0) {
       ptx::mbar_wait(bar_dfull, 0);
@@ -410,9 +430,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     }
     if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
     float* part = reinterpret_cast<float*>(smem);  // [BN][128] fp32 (split-K only)
-    const int jmax = S == 1 ? min(BN, M - m0) : BN;   // columns (tokens) worth reading
+    const int jmax = S == 1 ? min(j0 + kColsPerWarp, M - m0) : j0 + kColsPerWarp;
 #pragma unroll 1
-    for (int jc = 0; jc < jmax; jc += 8) {
+    for (int jc = j0; jc < jmax; jc += 8) {
       uint32_t v[8];
       if (na > 0) {
         ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + jc, v);
