@@ -762,11 +762,13 @@ struct Plan {
   int tile_n, split, ctas;
 };
 
-int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256; }
+// tile 256 (1 CTA/SM, 2-stage ring) measured slower than tile 128 at every M >= 128 on B200
+// (tools/tune_plan.py), so the automatic plan tiles large M by 128 tokens
+int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128; }
 
 // Launch plan (tuned with tools/tune_plan.py on B200):
-//  - tokens per tile: the smallest MMA N covering M (weights are dequantized once per m-tile,
-//    so larger M uses the widest tile; M > 256 tiles the tokens by 256);
+//  - tokens per tile: the smallest MMA N covering M, at most 128 (weights are dequantized once
+//    per m-tile; M > 128 tiles the tokens by 128);
 //  - split-K: the largest S <= 8 such that all tiles x S CTAs are resident in one wave (TMEM
 //    and shared memory allow 2 CTAs/SM up to tile 128, 1 above; clusters are GPC-placed, so
 //    residency is queried, not computed) and every CTA keeps >= 4 stages of K.
