@@ -1,0 +1,72 @@
+"""Tensor-parallel layers on the GPU (single-process NCCL group; marker: gpu).  The multi-rank
+collective pattern itself is covered on CPU by tests/test_tp.py (gloo, world size 2)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no GPU", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+from paper_2402_10076_b200 import quick, tp  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    yield
+    dist.destroy_process_group()
+
+
+def _x(p):
+    return torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
+
+
+def test_column_parallel_layer(nccl_world1):
+    p = synth.make_problem(31, M=12, N=1024, K=2048, G=128)
+    layer = tp.ColumnParallelW4A16(p.qweight, p.scales, p.zeros, 128)
+    y = layer.forward(_x(p))
+    torch.cuda.synchronize()
+    ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+    assert oracle.tol_check(y.float().cpu().numpy(), ref)["ok"]
+
+
+def test_row_parallel_layer_fp32_reduce(nccl_world1):
+    p = synth.make_problem(32, M=12, N=512, K=4096, G=128)
+    layer = tp.RowParallelW4A16(p.qweight, p.scales, p.zeros, 128)
+    y = layer.forward(_x(p)[:, layer.k0:layer.k1].contiguous())
+    torch.cuda.synchronize()
+    ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+    assert oracle.tol_check(y.float().cpu().numpy(), ref)["ok"]
+
+
+def test_gather_columns_matches_column_slices():
+    """The permutation the column-parallel epilogue applies, on slices computed per 'rank'."""
+    p = synth.make_problem(33, M=7, N=1024, K=1024, G=128)
+    P = 4
+    x = _x(p)
+    gathered = torch.empty((P, 7, 256), device="cuda", dtype=torch.float16)
+    for r in range(P):
+        qw, sc, zr = tp.shard_awq_columns(p.qweight, p.scales, p.zeros, r, P)
+        blob = torch.from_numpy(quick.quick_pack_weights(qw, sc, zr, 128)).cuda()
+        quick.quick_w4a16_gemm(x, blob, 256, 1024, 128, out=gathered[r])
+    y = quick.quick_gather_columns(gathered, P, 7, 256)
+    full = quick.quick_w4a16_gemm(x, torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, 128)).cuda(),
+                                  1024, 1024, 128)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), full.view(torch.int16))   # column shards change no arithmetic
