@@ -387,19 +387,26 @@ def oracle_step_sample(workload, budget_s):
         zr = synth.make_zeros(si, K, N, G)
         probs.append((N, K, qw, sc, zr))
 
+    xs = {(K, M): synth.make_x(1000 + M, M, K) for (N, K, *_r) in probs for M in Ms}
+
     def one(ns):
         fl = 0
         t0 = time.perf_counter()
         for (N, K, qw, sc, zr) in probs:
             n = min(ns, N)
             for M in Ms:
-                x = synth.make_x(1000 + M, M, K)
-                oracle.w4a16_reference(x, qw[:, :n // 8], sc[:, :n], zr[:, :n // 8], G)
+                oracle.w4a16_reference(xs[(K, M)], qw[:, :n // 8], sc[:, :n], zr[:, :n // 8], G)
                 fl += 2 * M * n * K
         return time.perf_counter() - t0, fl
 
-    t, fl = one(8)                                        # calibrate on 8 columns
-    ns = int(max(8, min(max(N for N, *_ in probs), (budget_s / max(t, 1e-6)) * 8)) // 8 * 8)
+    N_max = max(N for N, *_ in probs)
+    ns, t = 64, 0.0
+    while True:                                           # calibrate: grow the sample geometrically
+        t, _ = one(ns)
+        if t >= budget_s / 4 or ns >= N_max:
+            break
+        ns *= 2
+    ns = int(max(8, min(N_max, ns * budget_s / max(t, 1e-6))) // 8 * 8)
     return ns, one
 
 
