@@ -764,6 +764,8 @@ struct Plan {
 
 // tile 256 (1 CTA/SM, 2-stage ring) measured slower than tile 128 at every M >= 128 on B200
 // (tools/tune_plan.py), so the automatic plan tiles large M by 128 tokens
+constexpr int kMaxAccumK = 8192;
+
 int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128; }
 
 // Launch plan (tuned with tools/tune_plan.py on B200):
@@ -788,6 +790,11 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
       if (tiles > max_resident(tn, s2)) continue;
       S = s2;
     }
+    // accuracy: one TMEM fp32 accumulator sums at most kMaxAccumK of K (the tensor-core
+    // accumulation error grows with the summed length; at K = 28672 a single accumulator
+    // exceeds the 1e-2 relative bound near |y| = 1e-2)
+    const int s_min = (K + kMaxAccumK - 1) / kMaxAccumK;
+    if (S < s_min) S = std::min(s_min, quick::kMaxSplit);
   }
   return Plan{tn, S, tiles * S};
 }
