@@ -334,10 +334,15 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     const int p = (warp - 2) >> 2;       // parity of the A stages this warp dequantizes
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
-    const uint8_t* wrow = smem + C::W_OFF + r * 16;
-    const uint8_t* mrow = smem + C::M_OFF + r * 2;           // scale of row r in a meta block
-    const uint8_t* zrow = smem + C::M_OFF + 256 + (r >> 1);  // zero byte of row r
+    // 32-bit shared-window addresses: explicit ld.shared (a generic pointer through the
+    // 1 KiB alignment cast compiles to slower generic LD.E)
+    const uint32_t wrow = sbase + C::W_OFF + r * 16;
+    const uint32_t mrow = sbase + C::M_OFF + r * 2;           // scale of row r in a meta block
+    const uint32_t zrow = sbase + C::M_OFF + 256 + (r >> 1);  // zero byte of row r
     const uint32_t zsh = (uint32_t)(r & 1) * 4u;
+    auto consts_at = [&](uint32_t mo) {
+      return make_consts(ptx::lds_u16(mrow + mo), (ptx::lds_u8(zrow + mo) >> zsh) & 0xFu);
+    };
     const bool tw = TRACE && (warp == 2 && lane == 0);
     const bool g_big = (G % kKA) == 0;    // a group spans whole A stages
     uint32_t a_regs[32];
@@ -351,15 +356,15 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       ptx::mbar_wait(bar_full + 8 * slot, (uint32_t)((l / STAGES) & 1));
       if (tw) stamp(2, a);
       const int g0 = group_of(ka - sub * kKA);
-      const uint8_t* wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
+      const uint32_t wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
       const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
       const bool full_stage = (ka + kKA) <= k_end;
       uint4 w[4];
-      w[0] = *reinterpret_cast<const uint4*>(wp);
-      w[1] = *reinterpret_cast<const uint4*>(wp + kChunkBytes);
+      w[0] = ptx::lds128(wp);
+      w[1] = ptx::lds128(wp + kChunkBytes);
       if (full_stage) {
-        w[2] = *reinterpret_cast<const uint4*>(wp + 2 * kChunkBytes);
-        w[3] = *reinterpret_cast<const uint4*>(wp + 3 * kChunkBytes);
+        w[2] = ptx::lds128(wp + 2 * kChunkBytes);
+        w[3] = ptx::lds128(wp + 3 * kChunkBytes);
       } else {
         w[2] = make_uint4(0, 0, 0, 0);
         w[3] = w[2];
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         const int g = group_of(ka);
         if (g != g_prev) {
           const uint32_t mo = moff + (uint32_t)(g - g0) * kMetaBytes;
-          cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo), (zrow[mo] >> zsh) & 0xFu);
+          cst = consts_at(mo);
           g_prev = g;
         }
       }
@@ -376,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       if (!g_big) {
         const uint32_t mo0 = moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes;
         const uint32_t mo1 = moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes;
-        cst = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo0), (zrow[mo0] >> zsh) & 0xFu);
-        cst1 = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo1), (zrow[mo1] >> zsh) & 0xFu);
+        cst = consts_at(mo0);
+        cst1 = consts_at(mo1);
       }
       // this warp reads exactly one A stage of each load stage it touches
       ptx::mbar_arrive(bar_empty + 8 * slot);
@@ -401,8 +406,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         if (!g_big) {
           const uint32_t mo2 = moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes;
           const uint32_t mo3 = moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes;
-          cst2 = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo2), (zrow[mo2] >> zsh) & 0xFu);
-          cst3 = make_consts(*reinterpret_cast<const uint16_t*>(mrow + mo3), (zrow[mo3] >> zsh) & 0xFu);
+          cst2 = consts_at(mo2);
+          cst3 = consts_at(mo3);
         }
         uint32_t b_regs[32];
         dequant_word(w[2].x, cst2, b_regs + 0);
@@ -429,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
       ptx::tc_fence_after();
     }
     if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
-    float* part = reinterpret_cast<float*>(smem);  // [BN][128] fp32 (split-K only)
+    const uint32_t part = sbase;  // [BN][128] fp32 partial tile (split-K only), shared window
     const int jmax = S == 1 ? min(j0 + kColsPerWarp, M - m0) : j0 + kColsPerWarp;
 #pragma unroll 1
     for (int jc = j0; jc < jmax; jc += 8) {
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) part[(jc + i) * kTileRows + r] = __uint_as_float(v[i]);
+        for (int i = 0; i < 8; ++i) ptx::sts_u32(part + (uint32_t)(((jc + i) * kTileRows + r) * 4), v[i]);
       }
     }
   }
