@@ -229,6 +229,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     if (TRACE && tr != nullptr && i < kTraceStages) tr[8 + ev * kTraceStages + i] = clock64();
   };
   if (TRACE && tr != nullptr && threadIdx.x == 0) tr[0] = clock64();
+  unsigned long long t_start_ns = 0;
+  if (TRACE && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
   // let the next kernel in the stream launch its prologue early (PDL); it still waits for
   // this grid's completion before touching anything this grid writes
   ptx::griddep_launch_dependents();
@@ -512,6 +514,18 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (TRACE && threadIdx.x == 0) {
+    // all CTAs: (smid, start ns, end ns) after the 16 detailed records
+    unsigned long long t_end_ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end_ns));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const size_t lin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    unsigned long long* rec = trace + 16 * (size_t)kTraceStride + 3 * lin;
+    rec[0] = smid;
+    rec[1] = t_start_ns;
+    rec[2] = t_end_ns;
+  }
   if (TRACE && tr != nullptr && threadIdx.x == 0) {
     tr[2] = clock64();
     tr[3] = (unsigned long long)na;

@@ -22,7 +22,8 @@ blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G
 copies = [blob.clone() for _ in range(max(4, int(3e8 // blob.numel())))]
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((M, N), device="cuda", dtype=torch.float16)
-tr = torch.zeros(16 * STRIDE, dtype=torch.int64, device="cuda")
+NCTA = quick.quick_gemm_plan(M, N, K, G)["num_ctas"] if not (tn or sk) else 4096
+tr = torch.zeros(16 * STRIDE + 3 * max(NCTA, 4096), dtype=torch.int64, device="cuda")
 for i in range(3):
     quick.quick_w4a16_gemm(x, copies[i], N, K, G, out=y, tile_n=tn, split_k=sk)
 torch.cuda.synchronize()
@@ -30,7 +31,22 @@ lib.quick_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
 quick.quick_w4a16_gemm(x, copies[-1], N, K, G, out=y, tile_n=tn, split_k=sk)
 torch.cuda.synchronize()
 lib.quick_debug_set_trace(ctypes.c_void_p(0))
-t = tr.cpu().numpy().reshape(16, STRIDE)
+tt = tr.cpu().numpy()
+t = tt[:16 * STRIDE].reshape(16, STRIDE)
+rec = tt[16 * STRIDE:].reshape(-1, 3)
+rec = rec[rec[:, 1] > 0]
+if len(rec):
+    t0 = rec[:, 1].min()
+    span = (rec[:, 2].max() - t0) / 1e3
+    per_sm = {}
+    for smid, a, b in rec:
+        per_sm.setdefault(int(smid), []).append(((a - t0) / 1e3, (b - t0) / 1e3))
+    cnt = np.bincount([len(v) for v in per_sm.values()])
+    busy = np.array([max(b for _, b in v) for v in per_sm.values()])
+    dur = (rec[:, 2] - rec[:, 1]) / 1e3
+    print(f"ALL CTAs: {len(rec)} on {len(per_sm)} SMs, CTAs/SM histogram {cnt.tolist()}, kernel span {span:.2f} us, "
+          f"CTA duration min/med/max {dur.min():.2f}/{np.median(dur):.2f}/{dur.max():.2f} us, SM finish min/med/max "
+          f"{busy.min():.2f}/{np.median(busy):.2f}/{busy.max():.2f} us, start skew max {(rec[:,1].max()-t0)/1e3:.2f} us")
 print("plan", quick.quick_gemm_plan(M, N, K, G), "tile", tn, "split", sk)
 names = ["P_before_empty", "P_issued", "D_full", "D_aempty_ok", "D_afull_arrived", "M_afull_ok", "M_committed"]
 for c in range(16):
