@@ -59,8 +59,11 @@ quick_status_t quick_pack_weights(const uint32_t* qweight, const uint16_t* scale
 quick_status_t quick_unpack_weights(const void* packed, int group_size, int K, int N,
                                     uint32_t* qweight, uint16_t* scales, uint32_t* zeros);
 
-/* The hot path (device, asynchronous on `stream`; no allocation, no host sync, CUDA-graph
- * capturable).  Y = X . dequant(Wq) with fp32 accumulation (reading R4) and fp16 output.
+/* The hot path (device, asynchronous on `stream`; CUDA-graph capturable).  Y = X . dequant(Wq)
+ * with fp32 accumulation (reading R4) and fp16 output.  Small-M plans use a stream-K schedule
+ * whose fp32 partial tiles live in a per-(device, stream) workspace the library allocates on the
+ * first such call made outside graph capture (a few MiB; kept for the process lifetime); under
+ * capture without that workspace the cluster split-K plan (no workspace) is used instead.
  *   X       device, __half [M][K] row-major, 16-byte aligned
  *   packed  device copy of the quick_pack_weights blob, 128-byte aligned
  *   Y       device, __half [M][N] row-major, 16-byte aligned
@@ -75,20 +78,22 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
                                 kernel in the stream; X is read and Y written only after that
                                 kernel completes.  The weights must not be written by the
                                 immediately preceding kernel. */
+#define QUICK_FLAG_NO_STREAMK 4 /* never use the stream-K schedule (tests / A-B timing) */
 
 /* Extended form used by tensor parallelism, layer stacks and the tests.
  *   ldy       row stride of Y in elements (>= N, multiple of 8); lets a rank write its column
  *             slice of a wider Y in place
  *   flags     QUICK_FLAG_* bits (0 = fp16 Y, ordinary stream ordering)
  *   tile_n    tokens per MMA tile (16, 32, 64, 128, 256), 0 = automatic
- *   split_k   CTAs per cluster splitting K (1..8, <= K/64), 0 = automatic
+ *   split_k   CTAs per cluster splitting K (1..8, <= ceil(K/128)), 0 = automatic (which may
+ *             choose stream-K for tiles <= 64)
  * Deterministic: equal inputs and equal (tile_n, split_k) give bit-equal Y. */
 quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K,
                                    int group_size, void* Y, int ldy, int flags, int tile_n,
                                    int split_k, void* stream);
 
-/* The launch plan the automatic dispatch would use for (M, N, K, G): tokens per tile,
- * split-K factor and number of CTAs.  Any out pointer may be NULL. */
+/* The launch plan the automatic dispatch would use for (M, N, K, G): tokens per tile, cluster
+ * split-K factor (0 = stream-K schedule) and number of CTAs.  Any out pointer may be NULL. */
 quick_status_t quick_gemm_plan(int M, int N, int K, int group_size, int* tile_n, int* split_k,
                                int* num_ctas);
 

@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/quick.h"
 #include "quick_ptx.cuh"
@@ -39,6 +40,7 @@
 namespace quick {
 
 constexpr int kThreads = 320;     // 10 warps: producer, MMA, 8 dequantizers (2 per TMEM lane quarter)
+constexpr int kDqThreads = 256;   // the 8 dequantizer warps (named barrier 1 in stream-K epilogues)
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
 constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
@@ -48,15 +50,18 @@ constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable cluste
 constexpr int kTraceStages = 256; // debug tracing: stages recorded per traced CTA
 constexpr int kTraceStride = 8 + 7 * kTraceStages;
 
-// Per tile width BN (tokens per MMA): KL = k per load stage (one bulk copy of KL x 64 B of
-// weights, one bulk copy of the groups' metadata, one 3-D TMA of the [KL/64][BN][64] X tile),
-// STAGES = depth of the load ring.  Few, large async copies per byte: each TMA/bulk issue
-// costs ~150 SM cycles on B200 (measured with tools/trace_gemm.py).
-template <int BN>
+// Per tile width BN (tokens per MMA) and mode SK (stream-K):
+//   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
+//          metadata, one 3-D TMA of the [KL/64][BN][64] X tile (few, large async copies: each
+//          TMA/bulk issue costs ~150 SM cycles on B200, measured with tools/trace_gemm.py)
+//   STAGES depth of the load ring
+//   TMEM   A ring of ASTAGES x 64 columns, then NDBUF fp32 accumulators of BN columns (stream-K
+//          double-buffers D so a segment's epilogue overlaps the next segment's MMAs)
+template <int BN, bool SK>
 struct Cfg {
-  // TMEM: A ring (ASTAGES x 64 columns) then the fp32 accumulator (BN columns); 3 A stages fit
-  // in a 256-column allocation up to BN = 64 (2 CTAs per SM), 2 above
-  static constexpr int ASTAGES = BN <= 64 ? 3 : 2;
+  static constexpr int NDBUF = SK ? 2 : 1;
+  static constexpr int ASTAGES =
+      BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2);
   static constexpr int DCOL = ASTAGES * kAColsPerStage;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
@@ -69,22 +74,103 @@ struct Cfg {
   static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
   static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
   static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
-  // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 1;
-  static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;
+  // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull[2], dempty[2]
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 4;
+  static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;   // TMEM base, then stream-K flag
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = (DCOL + BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (DCOL + NDBUF * BN <= 256) ? 256 : 512;
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
   static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
   static constexpr int MIN_SMEM = (228 * 1024) / (MAX_CTAS_PER_SM + 1) + 1024;
   static constexpr int SMEM_BYTES = (USED + 1024 > MIN_SMEM ? USED + 1024 : MIN_SMEM);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
-  static_assert(KL % kKA == 0, "load stage = whole A stages");
+  static_assert(KL % kKA == 0 && APL <= 2, "load stage = one or two A stages");
+  static_assert(!SK || BN <= 64, "stream-K is used for the small-M tiles");
+  static_assert(DCOL + NDBUF * BN <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // split-K partial tile [BN][128] fp32 reuses the pipeline buffers once the mainloop is done
   static_assert(BN * kTileRows * 4 <= BAR_OFF, "split-K partial must fit in the pipeline smem");
 };
+
+// Kernel parameters (passed by value as a __grid_constant__).
+struct KParams {
+  const uint8_t* packed;
+  void* Y;
+  int M, N, K, G, g_shift, ldy, flags;
+  int n_tiles, m_tiles;   // tile index = t * m_tiles + mt (n-tile major: a CTA's tiles share weights)
+  int NA;                 // A stages (128 k) per tile: ceil(K / 128)
+  // stream-K (gridDim = (P, 1, 1)): CTA c owns units [c U / P, (c+1) U / P) of the U = tiles x NA
+  // (tile, A stage) units; partial tiles go through ws and are summed by the last arriver
+  long long U;
+  int P;
+  float* ws;              // [P][2][BN][128] fp32 partial tiles (slot 0: first segment, 1: last)
+  int* sems;              // [tiles] arrival counters, zero between launches (self-resetting)
+  unsigned long long* trace;
+};
+
+// One contiguous run of A stages [a_lo, a_hi) of one tile (n-tile t, m-tile mt).
+struct Seg {
+  int tile, t, mt, a_lo, a_hi;
+};
+
+// Enumerates this CTA's segments.  Cluster split-K: exactly one (blockIdx.y, blockIdx.z, the
+// split's A range).  Stream-K: the unit range of CTA blockIdx.x, cut at tile boundaries.
+struct SegIter {
+  long long u, u1;
+  int NA, m_tiles;
+  bool sk, done;
+  int t, mt, a_lo, a_hi;
+  __device__ __forceinline__ SegIter(const KParams& p, bool sk_) {
+    sk = sk_;
+    NA = p.NA;
+    m_tiles = p.m_tiles;
+    done = false;
+    if (sk) {
+      u = ((long long)blockIdx.x * p.U) / p.P;
+      u1 = ((long long)(blockIdx.x + 1) * p.U) / p.P;
+    } else {
+      const int S = gridDim.x;
+      t = blockIdx.y;
+      mt = blockIdx.z;
+      a_lo = (int)(((long long)blockIdx.x * NA) / S);
+      a_hi = (int)(((long long)(blockIdx.x + 1) * NA) / S);
+      u = u1 = 0;
+    }
+  }
+  __device__ __forceinline__ bool next(Seg& s) {
+    if (!sk) {
+      if (done) return false;
+      done = true;
+      s.t = t;
+      s.mt = mt;
+      s.tile = t * m_tiles + mt;
+      s.a_lo = a_lo;
+      s.a_hi = a_hi;
+      return a_hi > a_lo;
+    }
+    if (u >= u1) return false;
+    const long long tile = u / NA;
+    const int a0 = (int)(u - tile * NA);
+    const long long rem = u1 - u;
+    const int a1 = (rem < (long long)(NA - a0)) ? a0 + (int)rem : NA;
+    s.tile = (int)tile;
+    s.t = (int)(tile / m_tiles);
+    s.mt = (int)(tile - (long long)s.t * m_tiles);
+    s.a_lo = a0;
+    s.a_hi = a1;
+    u += (a1 - a0);
+    return true;
+  }
+};
+
+// stream-K bookkeeping: CTA owning unit u, and a CTA's first unit
+__device__ __forceinline__ int sk_cta_of(long long u, long long U, int P) {
+  return (int)(((u + 1) * P - 1) / U);
+}
+__device__ __forceinline__ long long sk_start(int c, long long U, int P) {
+  return ((long long)c * U) / P;
+}
 
 // ------------------------------------------------------------------------------------------
 // Dequantization of one 32-bit word of the v1 layout (8 codes, nibble order {0,2,4,6,1,3,5,7}
@@ -158,13 +244,11 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
 }
 
-template <int BN, bool TRACE>
-__global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
+template <int BN, bool SK, bool TRACE>
+__global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                          const uint8_t* __restrict__ packed, void* __restrict__ Y, int M, int N,
-                          int K, int G, int g_shift, int ldy, int flags,
-                          unsigned long long* __restrict__ trace) {
-  using C = Cfg<BN>;
+                          const __grid_constant__ KParams p) {
+  using C = Cfg<BN, SK>;
   constexpr int STAGES = C::STAGES;
   constexpr int APL = C::APL;
   constexpr int kAStages = C::ASTAGES;
@@ -175,22 +259,13 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   const uint32_t sbase = ptx::smem_u32(smem);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-
-  const int S = gridDim.x;            // split-K factor (= cluster size)
-  const int split = blockIdx.x;
-  const int t = blockIdx.y;           // n-tile
-  const int m0 = blockIdx.z * BN;     // first token of this tile
-  // K is split over the cluster in whole A stages (128 k; the last one of K may hold 64)
-  const int NA = (K + kKA - 1) / kKA;
-  const int a_begin = (int)(((long long)split * NA) / S);
-  const int na = (int)(((long long)(split + 1) * NA) / S) - a_begin;   // A stages of this CTA
-  const int k_begin = a_begin * kKA;
-  const int k_end = min(k_begin + na * kKA, K);
-  const int nl = (na + APL - 1) / APL;                                   // load stages
+  const int K = p.K, G = p.G, M = p.M;
+  const int S = SK ? 1 : (int)gridDim.x;   // cluster split-K factor
   const int C32 = K / 32;
   const int NG = K / G;
-  const bool out_fp32 = (flags & QUICK_FLAG_OUT_F32) != 0;
-  const bool pdl = (flags & QUICK_FLAG_PDL) != 0;
+  const bool out_fp32 = (p.flags & QUICK_FLAG_OUT_F32) != 0;
+  const bool pdl = (p.flags & QUICK_FLAG_PDL) != 0;
+  const int g_shift = p.g_shift;
   // group index of k: shift when G is a power of two, division otherwise
   auto group_of = [&](int k) { return g_shift >= 0 ? (k >> g_shift) : (k / G); };
 
@@ -198,21 +273,26 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   const uint32_t bar_empty = bar_full + 8 * STAGES;
   const uint32_t bar_afull = bar_empty + 8 * STAGES;
   const uint32_t bar_aempty = bar_afull + 8 * kAStages;
-  const uint32_t bar_dfull = bar_aempty + 8 * kAStages;
+  const uint32_t bar_dfull = bar_aempty + 8 * kAStages;   // [2]
+  const uint32_t bar_dempty = bar_dfull + 16;             // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::HOLD_OFF);
+  volatile int* sk_flag = reinterpret_cast<volatile int*>(smem + C::HOLD_OFF + 4);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
-      // every thread of the dequant warps reading this load stage (both parities when it holds
-      // two A stages, one parity otherwise) + 1 MMA commit
-      ptx::mbar_init(bar_empty + 8 * s, 4 * 32 * (APL >= 2 ? 2 : 1) + 1);
+      // 128 dequant-thread arrivals per A stage of the load stage (a thread reading the only A
+      // stage of a short load stage arrives for both) + 1 MMA commit
+      ptx::mbar_init(bar_empty + 8 * s, 4 * 32 * APL + 1);
     }
     for (int a = 0; a < kAStages; ++a) {
       ptx::mbar_init(bar_afull + 8 * a, 4 * 32);      // every thread of one parity group
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
-    ptx::mbar_init(bar_dfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(bar_dfull + 8 * b, 1);
+      ptx::mbar_init(bar_dempty + 8 * b, kDqThreads);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
@@ -223,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   const uint32_t tmem = *tmem_holder;
   // debug tracing (TRACE instantiation only, tools/trace_gemm.py): clock64 stamps per stage
   unsigned long long* tr = nullptr;
-  if (TRACE && blockIdx.z == 0 && blockIdx.y < 2)
-    tr = trace + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * kTraceStride;
+  const unsigned lin16 = SK ? blockIdx.x : blockIdx.y * gridDim.x + blockIdx.x;
+  if (TRACE && blockIdx.z == 0 && lin16 < 16) tr = p.trace + (size_t)lin16 * kTraceStride;
   auto stamp = [&](int ev, int i) {
     if (TRACE && tr != nullptr && i < kTraceStages) tr[8 + ev * kTraceStages + i] = clock64();
   };
@@ -238,46 +318,53 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
     // The whole warp runs the (warp-uniform) loop; one elected lane issues the copies, so the
-    // addresses stay in uniform registers and no per-lane waterfall is generated.
+    // addresses stay in uniform registers and no per-lane waterfall is generated.  Load
+    // stages never straddle segments (the last one of a segment may be short).
     const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
-    const uint8_t* wbase = packed + (size_t)t * C32 * kChunkBytes;
-    const uint8_t* mbase = packed + (size_t)K * N / 2 + (size_t)t * NG * kMetaBytes;
-    // Weights and metadata are read-only for this call: their bulk copies may be issued
-    // before the programmatic grid dependency resolves; X may be produced by the previous
-    // kernel, so its TMA waits for it (PDL).
-    const int pre = pdl ? (nl < STAGES ? nl : STAGES) : 0;
-    int slot = 0;
+    SegIter it(p, SK);
+    Seg sg;
+    int slot = 0, lf = 0;
     uint32_t ph = 0;
-    for (int l = 0; l < nl; ++l) {
-      const int kl0 = k_begin + l * C::KL;
-      const int kv = min(C::KL, k_end - kl0);          // valid k in this load stage
-      if (lane == 0) stamp(0, l);
-      if (l >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
-      const int g0 = group_of(kl0);
-      const uint32_t meta_bytes = (uint32_t)(group_of(kl0 + kv - 1) - g0 + 1) * kMetaBytes;
-      const uint32_t full = bar_full + 8 * slot;
-      if (ptx::elect_one()) {
-        ptx::mbar_arrive_expect_tx(full, C::X_BYTES + (uint32_t)kv * 64u + meta_bytes);
-        ptx::bulk_load_hint(sbase + C::W_OFF + slot * C::W_BYTES,
-                            wbase + (size_t)(kl0 / 32) * kChunkBytes, (uint32_t)kv * 64u, full, pol_w);
-        ptx::bulk_load_hint(sbase + C::M_OFF + slot * C::M_BYTES, mbase + (size_t)g0 * kMetaBytes,
-                            meta_bytes, full, pol_w);
-        if (l >= pre && !(pre == 0 && l == 0)) {
-          ptx::tma_load_3d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, 0, m0, kl0 / 64, full,
-                                pol_x);
-        } else if (l == (pre > 0 ? pre - 1 : 0)) {
-          if (pdl) ptx::griddep_wait();
-          for (int j = 0; j <= l; ++j)   // X of the stages issued so far (weights went first)
-            ptx::tma_load_3d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, 0, m0,
-                                  (k_begin + j * C::KL) / 64, bar_full + 8 * j, pol_x);
+    int pre = -1;   // PDL: weight copies of the first `pre` load stages go before the X wait
+    while (it.next(sg)) {
+      const uint8_t* wbase = p.packed + (size_t)sg.t * C32 * kChunkBytes;
+      const uint8_t* mbase = p.packed + (size_t)K * p.N / 2 + (size_t)sg.t * NG * kMetaBytes;
+      const int m0 = sg.mt * BN;
+      const int k_seg_end = min(sg.a_hi * kKA, K);
+      const int nl = (sg.a_hi - sg.a_lo + APL - 1) / APL;
+      if (pre < 0) pre = pdl ? (nl < STAGES ? nl : STAGES) : 0;
+      for (int l = 0; l < nl; ++l, ++lf) {
+        const int kl0 = (sg.a_lo + l * APL) * kKA;
+        const int kv = min(C::KL, k_seg_end - kl0);   // valid k in this load stage
+        if (lane == 0) stamp(0, lf);
+        if (lf >= pre) ptx::mbar_wait(bar_empty + 8 * slot, ph ^ 1u);
+        const int g0 = group_of(kl0);
+        const uint32_t meta_bytes = (uint32_t)(group_of(kl0 + kv - 1) - g0 + 1) * kMetaBytes;
+        const uint32_t full = bar_full + 8 * slot;
+        if (ptx::elect_one()) {
+          ptx::mbar_arrive_expect_tx(full, C::X_BYTES + (uint32_t)kv * 64u + meta_bytes);
+          ptx::bulk_load_hint(sbase + C::W_OFF + slot * C::W_BYTES,
+                              wbase + (size_t)(kl0 / 32) * kChunkBytes, (uint32_t)kv * 64u, full,
+                              pol_w);
+          ptx::bulk_load_hint(sbase + C::M_OFF + slot * C::M_BYTES,
+                              mbase + (size_t)g0 * kMetaBytes, meta_bytes, full, pol_w);
+          if (lf >= pre && !(pre == 0 && lf == 0)) {
+            ptx::tma_load_3d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, 0, m0, kl0 / 64,
+                                  full, pol_x);
+          } else if (lf == (pre > 0 ? pre - 1 : 0)) {
+            if (pdl) ptx::griddep_wait();
+            for (int j = 0; j <= lf; ++j)   // X of the stages issued so far (all in this segment)
+              ptx::tma_load_3d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, 0, m0,
+                                    (sg.a_lo + j * APL) * kKA / 64, bar_full + 8 * j, pol_x);
+          }
         }
-      }
-      __syncwarp();
-      if (lane == 0) stamp(1, l);
-      if (++slot == STAGES) {
-        slot = 0;
-        ph ^= 1u;
+        __syncwarp();
+        if (lane == 0) stamp(1, lf);
+        if (++slot == STAGES) {
+          slot = 0;
+          ph ^= 1u;
+        }
       }
     }
   } else if (warp == 1) {
@@ -286,43 +373,55 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     // the async tcgen05 ops of the thread that issues it, so the same lane does both).
     constexpr uint32_t idesc = instr_desc<BN>();
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
-    int slot = 0, sub = 0, as = 0;
+    SegIter it(p, SK);
+    Seg sg;
+    int slot = 0, as = 0, si = 0, ia = 0;
     uint32_t aph = 0;
-    for (int a = 0; a < na; ++a) {
-      // A stage written by all 4 dequant warps; they waited on `full`, which also covers the
-      // X tile of this load stage, so one wait orders both operands
-      ptx::mbar_wait(bar_afull + 8 * as, aph);
-      if (lane == 0) stamp(5, a);
-      ptx::tc_fence_after();
-      const int kv = min(kKA, k_end - (k_begin + a * kKA));   // 128, or 64 at the end of K
-      if (ptx::elect_one()) {
-        const uint32_t a_col = tmem + as * kAColsPerStage;
-        // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
-        const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES + sub * 2 * C::X_SUB) >> 4);
+    while (it.next(sg)) {
+      const int db = SK ? (si & 1) : 0;
+      // stream-K: the accumulator of segment si - 2 must have been read out
+      if (SK && si >= 2) ptx::mbar_wait(bar_dempty + 8 * db, (uint32_t)(((si >> 1) + 1) & 1));
+      const uint32_t d_col = tmem + kDCol + (uint32_t)(db * BN);
+      int sub = 0;
+      for (int a = sg.a_lo; a < sg.a_hi; ++a, ++ia) {
+        // A stage written by the 4 warps of its parity group; they waited on `full`, which
+        // also covers the X tile of this load stage, so one wait orders both operands
+        ptx::mbar_wait(bar_afull + 8 * as, aph);
+        if (lane == 0) stamp(5, ia);
+        ptx::tc_fence_after();
+        const int kv = min(kKA, K - a * kKA);   // 128, or 64 at the end of K
+        const bool last_of_load = (sub == APL - 1) || (a == sg.a_hi - 1);
+        if (ptx::elect_one()) {
+          const uint32_t a_col = tmem + as * kAColsPerStage;
+          // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
+          const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES + sub * 2 * C::X_SUB) >> 4);
+          const bool first = (a == sg.a_lo);
 #pragma unroll
-        for (int kk = 0; kk < kKA / 16; ++kk) {
-          if (kk * 16 < kv)
-            ptx::mma_f16_ts(tmem + kDCol, a_col + kk * 8,
-                            dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
-                            (a | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < kKA / 16; ++kk) {
+            if (kk * 16 < kv)
+              ptx::mma_f16_ts(d_col, a_col + kk * 8,
+                              dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
+                              (first && kk == 0) ? 0u : 1u);
+          }
+          ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
+          if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage used
+          if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);  // segment accumulated
         }
-        ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
-        if (sub == APL - 1 || a == na - 1)
-          ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage consumed
+        __syncwarp();
+        if (lane == 0) stamp(6, ia);
+        if (last_of_load) {
+          sub = 0;
+          if (++slot == STAGES) slot = 0;
+        } else {
+          ++sub;
+        }
+        if (++as == kAStages) {
+          as = 0;
+          aph ^= 1u;
+        }
       }
-      __syncwarp();
-      if (lane == 0) stamp(6, a);
-      if (++sub == APL || a == na - 1) {
-        sub = 0;
-        if (++slot == STAGES) slot = 0;
-      }
-      if (++as == kAStages) {
-        as = 0;
-        aph ^= 1u;
-      }
+      ++si;
     }
-    if (ptx::elect_one()) ptx::mma_commit(bar_dfull);
-    __syncwarp();
   } else {
     // ------------------------------------------------------------------ dequantizers
     // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access) and takes the
@@ -331,9 +430,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     // row) loads 4 x 16 B = 128 codes and writes 64 TMEM columns in two tcgen05.st.32x32b.x32;
     // the second half is dequantized while the first store drains.  Group constants (s,
     // 1024 + z, -(64 + z)) are rebuilt only when the group changes (G % 128 == 0), or per
-    // 32-k chunk otherwise.  Every thread arrives on the barriers itself.
+    // 32-k chunk otherwise.  Every thread arrives on the barriers itself.  After each segment
+    // the same warps run its epilogue (their TMEM lanes, half of the columns each).
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int p = (warp - 2) >> 2;       // parity of the A stages this warp dequantizes
+    const int par = (warp - 2) >> 2;     // parity of the A stages this warp dequantizes
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
     // 32-bit shared-window addresses: explicit ld.shared (a generic pointer through the
@@ -347,131 +447,190 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     };
     const bool tw = TRACE && (warp == 2 && lane == 0);
     const bool g_big = (G % kKA) == 0;    // a group spans whole A stages
-    uint32_t a_regs[32];
-    int g_prev = -1;
-    DequantConsts cst = make_consts(0, 0);
-    for (int a = p; a < na; a += 2) {
-      const int ka = k_begin + a * kKA;
-      const int l = a / APL;               // load stage of this A stage
-      const int sub = a - l * APL;
-      const int slot = l % STAGES;
-      ptx::mbar_wait(bar_full + 8 * slot, (uint32_t)((l / STAGES) & 1));
-      if (tw) stamp(2, a);
-      const int g0 = group_of(ka - sub * kKA);
-      const uint32_t wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
-      const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
-      const bool full_stage = (ka + kKA) <= k_end;
-      uint4 w[4];
-      w[0] = ptx::lds128(wp);
-      w[1] = ptx::lds128(wp + kChunkBytes);
-      if (full_stage) {
-        w[2] = ptx::lds128(wp + 2 * kChunkBytes);
-        w[3] = ptx::lds128(wp + 3 * kChunkBytes);
-      } else {
-        w[2] = make_uint4(0, 0, 0, 0);
-        w[3] = w[2];
-      }
-      if (g_big) {
-        const int g = group_of(ka);
-        if (g != g_prev) {
-          const uint32_t mo = moff + (uint32_t)(g - g0) * kMetaBytes;
-          cst = consts_at(mo);
-          g_prev = g;
-        }
-      }
-      DequantConsts cst1 = cst;
-      if (!g_big) {
-        const uint32_t mo0 = moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes;
-        const uint32_t mo1 = moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes;
-        cst = consts_at(mo0);
-        cst1 = consts_at(mo1);
-      }
-      // this warp reads exactly one A stage of each load stage it touches
-      ptx::mbar_arrive(bar_empty + 8 * slot);
-      const int as = a % kAStages;
-      const uint32_t aph = (uint32_t)((a / kAStages) & 1);
-      dequant_word(w[0].x, cst, a_regs + 0);
-      dequant_word(w[0].y, cst, a_regs + 4);
-      dequant_word(w[0].z, cst, a_regs + 8);
-      dequant_word(w[0].w, cst, a_regs + 12);
-      dequant_word(w[1].x, cst1, a_regs + 16);
-      dequant_word(w[1].y, cst1, a_regs + 20);
-      dequant_word(w[1].z, cst1, a_regs + 24);
-      dequant_word(w[1].w, cst1, a_regs + 28);
-      ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
-      if (tw) stamp(3, a);
-      ptx::tc_fence_after();
-      const uint32_t acol = tmem + tlane + as * kAColsPerStage;
-      ptx::tmem_st_32x32b_x32(acol, a_regs);
-      if (full_stage) {
-        DequantConsts cst2 = cst, cst3 = cst;
-        if (!g_big) {
-          const uint32_t mo2 = moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes;
-          const uint32_t mo3 = moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes;
-          cst2 = consts_at(mo2);
-          cst3 = consts_at(mo3);
-        }
-        uint32_t b_regs[32];
-        dequant_word(w[2].x, cst2, b_regs + 0);
-        dequant_word(w[2].y, cst2, b_regs + 4);
-        dequant_word(w[2].z, cst2, b_regs + 8);
-        dequant_word(w[2].w, cst2, b_regs + 12);
-        dequant_word(w[3].x, cst3, b_regs + 16);
-        dequant_word(w[3].y, cst3, b_regs + 20);
-        dequant_word(w[3].z, cst3, b_regs + 24);
-        dequant_word(w[3].w, cst3, b_regs + 28);
-        ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
-      }
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(bar_afull + 8 * as);
-      if (tw) stamp(4, a);
-    }
-    // ------------------------------------------------------------------ epilogue part 1
     constexpr int kColsPerWarp = BN / 2;
-    const int j0 = p * kColsPerWarp;     // this warp's half of the accumulator columns
-    const int n = t * kTileRows + r;
-    if (na > 0) {
-      ptx::mbar_wait(bar_dfull, 0);
-      ptx::tc_fence_after();
-    }
-    if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
-    const uint32_t part = sbase;  // [BN][128] fp32 partial tile (split-K only), shared window
-    const int jmax = S == 1 ? min(j0 + kColsPerWarp, M - m0) : j0 + kColsPerWarp;
-#pragma unroll 1
-    for (int jc = j0; jc < jmax; jc += 8) {
-      uint32_t v[8];
-      if (na > 0) {
-        ptx::tmem_ld_32x32b_x8(tmem + tlane + kDCol + jc, v);
-        ptx::tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = 0u;
-      }
-      if (S == 1) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int m = m0 + jc + i;
-          if (m < M) {
-            const float f = __uint_as_float(v[i]);
-            if (out_fp32)
-              reinterpret_cast<float*>(Y)[(size_t)m * ldy + n] = f;
-            else
-              reinterpret_cast<__half*>(Y)[(size_t)m * ldy + n] = __float2half_rn(f);
+    const int j0 = par * kColsPerWarp;   // this warp's half of the accumulator columns
+    uint32_t a_regs[32];
+    SegIter it(p, SK);
+    Seg sg;
+    int ia = 0, si = 0, lbase = 0;       // flat A-stage index, segment index, first load stage
+    while (it.next(sg)) {
+      int g_prev = -1;                   // group constants are per tile: reset per segment
+      DequantConsts cst = make_consts(0, 0);
+      const int k_seg_end = min(sg.a_hi * kKA, K);
+      for (int a = sg.a_lo; a < sg.a_hi; ++a, ++ia) {
+        if ((ia & 1) != par) continue;
+        const int ka = a * kKA;
+        const int rel = a - sg.a_lo;
+        const int lf = lbase + rel / APL;        // flat load stage of this A stage
+        const int sub = rel - (rel / APL) * APL;
+        const int slot = lf % STAGES;
+        ptx::mbar_wait(bar_full + 8 * slot, (uint32_t)((lf / STAGES) & 1));
+        if (tw) stamp(2, ia);
+        const int g0 = group_of(ka - sub * kKA);
+        const uint32_t wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
+        const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
+        const bool full_stage = (ka + kKA) <= k_seg_end;
+        uint4 w[4];
+        w[0] = ptx::lds128(wp);
+        w[1] = ptx::lds128(wp + kChunkBytes);
+        if (full_stage) {
+          w[2] = ptx::lds128(wp + 2 * kChunkBytes);
+          w[3] = ptx::lds128(wp + 3 * kChunkBytes);
+        } else {
+          w[2] = make_uint4(0, 0, 0, 0);
+          w[3] = w[2];
+        }
+        if (g_big) {
+          const int g = group_of(ka);
+          if (g != g_prev) {
+            cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
+            g_prev = g;
           }
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ptx::sts_u32(part + (uint32_t)(((jc + i) * kTileRows + r) * 4), v[i]);
+        DequantConsts cst1 = cst;
+        if (!g_big) {
+          cst = consts_at(moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes);
+          cst1 = consts_at(moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes);
+        }
+        // one arrival per thread per A stage; a load stage holding a single A stage (end of a
+        // segment) gets the other parity's share from the same thread
+        const int in_load = min(APL, sg.a_hi - (a - sub));
+        ptx::mbar_arrive_cnt(bar_empty + 8 * slot, (uint32_t)(APL - in_load + 1));
+        const int as = ia % kAStages;
+        const uint32_t aph = (uint32_t)((ia / kAStages) & 1);
+        dequant_word(w[0].x, cst, a_regs + 0);
+        dequant_word(w[0].y, cst, a_regs + 4);
+        dequant_word(w[0].z, cst, a_regs + 8);
+        dequant_word(w[0].w, cst, a_regs + 12);
+        dequant_word(w[1].x, cst1, a_regs + 16);
+        dequant_word(w[1].y, cst1, a_regs + 20);
+        dequant_word(w[1].z, cst1, a_regs + 24);
+        dequant_word(w[1].w, cst1, a_regs + 28);
+        ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+        if (tw) stamp(3, ia);
+        ptx::tc_fence_after();
+        const uint32_t acol = tmem + tlane + as * kAColsPerStage;
+        ptx::tmem_st_32x32b_x32(acol, a_regs);
+        if (full_stage) {
+          DequantConsts cst2 = cst, cst3 = cst;
+          if (!g_big) {
+            cst2 = consts_at(moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes);
+            cst3 = consts_at(moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes);
+          }
+          uint32_t b_regs[32];
+          dequant_word(w[2].x, cst2, b_regs + 0);
+          dequant_word(w[2].y, cst2, b_regs + 4);
+          dequant_word(w[2].z, cst2, b_regs + 8);
+          dequant_word(w[2].w, cst2, b_regs + 12);
+          dequant_word(w[3].x, cst3, b_regs + 16);
+          dequant_word(w[3].y, cst3, b_regs + 20);
+          dequant_word(w[3].z, cst3, b_regs + 24);
+          dequant_word(w[3].w, cst3, b_regs + 28);
+          ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+        }
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar_afull + 8 * as);
+        if (tw) stamp(4, ia);
       }
+      lbase += (sg.a_hi - sg.a_lo + APL - 1) / APL;
+
+      // ---------------------------------------------------------------- segment epilogue
+      const int db = SK ? (si & 1) : 0;
+      const int m0 = sg.mt * BN;
+      const int n = sg.t * kTileRows + r;
+      ptx::mbar_wait(bar_dfull + 8 * db, (uint32_t)((si >> 1) & 1));
+      ptx::tc_fence_after();
+      if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
+      const uint32_t dcol = tmem + tlane + kDCol + (uint32_t)(db * BN);
+      const bool whole = SK ? (sg.a_lo == 0 && sg.a_hi == p.NA) : (S == 1);
+      const int jmax = min(j0 + kColsPerWarp, M - m0);   // valid tokens (columns)
+      if (whole) {
+        // the full K range of this tile is in our accumulator: straight to Y
+#pragma unroll 1
+        for (int jc = j0; jc < jmax; jc += 8) {
+          uint32_t v[8];
+          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int m = m0 + jc + i;
+            if (m < M) {
+              const float f = __uint_as_float(v[i]);
+              if (out_fp32)
+                reinterpret_cast<float*>(p.Y)[(size_t)m * p.ldy + n] = f;
+              else
+                reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(f);
+            }
+          }
+        }
+      } else if (!SK) {
+        // cluster split-K: fp32 partial tile [BN][128] into our shared memory (pipeline buffers
+        // are free: every stage has been consumed); reduced through DSMEM below
+#pragma unroll 1
+        for (int jc = j0; jc < j0 + kColsPerWarp; jc += 8) {
+          uint32_t v[8];
+          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            ptx::sts_u32(sbase + (uint32_t)(((jc + i) * kTileRows + r) * 4), v[i]);
+        }
+      } else {
+        // stream-K partial tile: fp32 into this CTA's workspace slot (0: first segment, 1: the
+        // last), then the last CTA to arrive on the tile sums every partial in CTA order
+        float* slot_ws = p.ws + ((size_t)blockIdx.x * 2 + (si == 0 ? 0 : 1)) * (BN * kTileRows);
+#pragma unroll 1
+        for (int jc = j0; jc < jmax; jc += 8) {
+          uint32_t v[8];
+          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (jc + i < jmax) __stcg(slot_ws + (jc + i) * kTileRows + r, __uint_as_float(v[i]));
+        }
+        const long long u_first = (long long)sg.tile * p.NA;
+        const int c_first = sk_cta_of(u_first, p.U, p.P);
+        const int c_last = sk_cta_of(u_first + p.NA - 1, p.U, p.P);
+        __threadfence();
+        ptx::named_bar_sync(1, kDqThreads);
+        if (threadIdx.x == 64) {
+          const int prev = atomicAdd(p.sems + sg.tile, 1);
+          *sk_flag = (prev == c_last - c_first) ? 1 : 0;
+        }
+        ptx::named_bar_sync(1, kDqThreads);
+        if (*sk_flag) {
+          __threadfence();
+#pragma unroll 1
+          for (int jc = j0; jc < jmax; ++jc) {
+            float acc = 0.f;
+            for (int c = c_first; c <= c_last; ++c) {
+              const int sl = (sk_start(c, p.U, p.P) >= u_first) ? 0 : 1;
+              acc += __ldcg(p.ws + ((size_t)c * 2 + sl) * (BN * kTileRows) + jc * kTileRows + r);
+            }
+            const int m = m0 + jc;
+            if (out_fp32)
+              reinterpret_cast<float*>(p.Y)[(size_t)m * p.ldy + n] = acc;
+            else
+              reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(acc);
+          }
+          if (threadIdx.x == 64) p.sems[sg.tile] = 0;   // self-reset for the next launch
+        }
+      }
+      if (SK) {
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar_dempty + 8 * db);
+      }
+      ++si;
     }
   }
 
-  if (S > 1) {
-    // ---------------------------------------------------------------- split-K reduction
+  if (!SK && S > 1) {
+    // ---------------------------------------------------------------- cluster split-K reduce
     // fixed order p = 0..S-1 over the cluster's fp32 partials: deterministic (reading R12).
     // All S DSMEM loads of an element are issued before the first add (latency ~200 cycles).
     ptx::cluster_sync();
+    const int m0 = blockIdx.z * BN;
     const uint32_t my = ptx::cluster_ctarank();
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
     const int eb = (int)(((int)my * E4) / S) * 4;
@@ -479,34 +638,33 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     const int e_lim = min(ee, max(0, (M - m0)) * kTileRows);   // skip padded tokens
     uint32_t peer[kMaxSplit];
 #pragma unroll
-    for (int p = 0; p < kMaxSplit; ++p) peer[p] = ptx::mapa(sbase, (uint32_t)(p < S ? p : 0));
+    for (int q = 0; q < kMaxSplit; ++q) peer[q] = ptx::mapa(sbase, (uint32_t)(q < S ? q : 0));
     for (int e = eb + (int)threadIdx.x * 4; e < e_lim; e += kThreads * 4) {
       float4 v[kMaxSplit];
 #pragma unroll
-      for (int p = 0; p < kMaxSplit; ++p)
-        if (p < S) v[p] = ptx::ld_dsmem_f32x4(peer[p] + (uint32_t)e * 4u);
+      for (int q = 0; q < kMaxSplit; ++q)
+        if (q < S) v[q] = ptx::ld_dsmem_f32x4(peer[q] + (uint32_t)e * 4u);
       float4 acc = v[0];
 #pragma unroll
-      for (int p = 1; p < kMaxSplit; ++p)
-        if (p < S) {
-          acc.x += v[p].x;
-          acc.y += v[p].y;
-          acc.z += v[p].z;
-          acc.w += v[p].w;
+      for (int q = 1; q < kMaxSplit; ++q)
+        if (q < S) {
+          acc.x += v[q].x;
+          acc.y += v[q].y;
+          acc.z += v[q].z;
+          acc.w += v[q].w;
         }
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
-      const int m = m0 + j;
-      const size_t o = (size_t)m * ldy + (size_t)t * kTileRows + rr;
+      const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)blockIdx.y * kTileRows + rr;
       if (out_fp32) {
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + o) = acc;
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
       } else {
         __half2 lo = __floats2half2_rn(acc.x, acc.y);
         __half2 hi = __floats2half2_rn(acc.z, acc.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(Y) + o) = pk;
+        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
       }
     }
     ptx::cluster_sync();   // peers may still be reading our partials
@@ -521,14 +679,18 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN>::MAX_CTAS_PER_SM)
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     const size_t lin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    unsigned long long* rec = trace + 16 * (size_t)kTraceStride + 3 * lin;
+    unsigned long long* rec = p.trace + 16 * (size_t)kTraceStride + 3 * lin;
     rec[0] = smid;
     rec[1] = t_start_ns;
     rec[2] = t_end_ns;
   }
   if (TRACE && tr != nullptr && threadIdx.x == 0) {
     tr[2] = clock64();
-    tr[3] = (unsigned long long)na;
+    int na_total = 0;
+    SegIter it(p, SK);
+    Seg sg;
+    while (it.next(sg)) na_total += sg.a_hi - sg.a_lo;
+    tr[3] = (unsigned long long)na_total;
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tr[4] = smid;
@@ -601,7 +763,7 @@ __global__ void quick_gather_columns_kernel(const uint4* __restrict__ src, uint4
 }  // namespace quick
 
 // ============================================================================================
-// Host side: validation, launch plan, tensor map, launch.
+// Host side: validation, launch plan, stream-K workspace, tensor map, launch.
 // ============================================================================================
 namespace {
 
@@ -666,99 +828,80 @@ quick_status_t check_gemm_shape(int M, int N, int K, int G) {
   return QUICK_OK;
 }
 
-template <int BN>
-void* kernel_ptr() {
-  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, false>);
-}
-void* kernel_for(int bn) {
-  switch (bn) {
-    case 16: return kernel_ptr<16>();
-    case 32: return kernel_ptr<32>();
-    case 64: return kernel_ptr<64>();
-    case 128: return kernel_ptr<128>();
-    default: return kernel_ptr<256>();
-  }
-}
-template <int BN>
-void* trace_kernel_ptr() {
-  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, true>);
-}
-void* trace_kernel_for(int bn) {
-  switch (bn) {
-    case 16: return trace_kernel_ptr<16>();
-    case 32: return trace_kernel_ptr<32>();
-    case 64: return trace_kernel_ptr<64>();
-    case 128: return trace_kernel_ptr<128>();
-    default: return trace_kernel_ptr<256>();
-  }
-}
-int tmem_cols_for(int bn) {
-  switch (bn) {
-    case 16: return quick::Cfg<16>::TMEM_COLS;
-    case 32: return quick::Cfg<32>::TMEM_COLS;
-    case 64: return quick::Cfg<64>::TMEM_COLS;
-    case 128: return quick::Cfg<128>::TMEM_COLS;
-    default: return quick::Cfg<256>::TMEM_COLS;
-  }
-}
-int kl_for(int bn) {
-  switch (bn) {
-    case 16: return quick::Cfg<16>::KL;
-    case 32: return quick::Cfg<32>::KL;
-    case 64: return quick::Cfg<64>::KL;
-    case 128: return quick::Cfg<128>::KL;
-    default: return quick::Cfg<256>::KL;
-  }
-}
-int smem_for(int bn) {
-  switch (bn) {
-    case 16: return quick::Cfg<16>::SMEM_BYTES;
-    case 32: return quick::Cfg<32>::SMEM_BYTES;
-    case 64: return quick::Cfg<64>::SMEM_BYTES;
-    case 128: return quick::Cfg<128>::SMEM_BYTES;
-    default: return quick::Cfg<256>::SMEM_BYTES;
-  }
-}
+// tile widths with a stream-K variant
+inline bool sk_capable(int bn) { return bn <= 64; }
 
-// one-time per (device, tile): opt into the dynamic shared memory the config needs
-cudaError_t configure_kernel(int bn) {
+template <int BN, bool SK, bool TRACE>
+void* kernel_ptr() {
+  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, SK, TRACE>);
+}
+template <bool TRACE>
+void* kernel_for_t(int bn, bool sk) {
+  switch (bn) {
+    case 16: return sk ? kernel_ptr<16, true, TRACE>() : kernel_ptr<16, false, TRACE>();
+    case 32: return sk ? kernel_ptr<32, true, TRACE>() : kernel_ptr<32, false, TRACE>();
+    case 64: return sk ? kernel_ptr<64, true, TRACE>() : kernel_ptr<64, false, TRACE>();
+    case 128: return kernel_ptr<128, false, TRACE>();
+    default: return kernel_ptr<256, false, TRACE>();
+  }
+}
+void* kernel_for(int bn, bool sk) { return kernel_for_t<false>(bn, sk); }
+void* trace_kernel_for(int bn, bool sk) { return kernel_for_t<true>(bn, sk); }
+
+#define QUICK_CFG_FIELD(FN, FIELD)                                                        \
+  int FN(int bn, bool sk) {                                                               \
+    switch (bn) {                                                                         \
+      case 16: return sk ? quick::Cfg<16, true>::FIELD : quick::Cfg<16, false>::FIELD;   \
+      case 32: return sk ? quick::Cfg<32, true>::FIELD : quick::Cfg<32, false>::FIELD;   \
+      case 64: return sk ? quick::Cfg<64, true>::FIELD : quick::Cfg<64, false>::FIELD;   \
+      case 128: return quick::Cfg<128, false>::FIELD;                                    \
+      default: return quick::Cfg<256, false>::FIELD;                                     \
+    }                                                                                     \
+  }
+QUICK_CFG_FIELD(tmem_cols_for, TMEM_COLS)
+QUICK_CFG_FIELD(kl_for, KL)
+QUICK_CFG_FIELD(smem_for, SMEM_BYTES)
+#undef QUICK_CFG_FIELD
+
+// one-time per (device, tile, mode): opt into the dynamic shared memory the config needs
+cudaError_t configure_kernel(int bn, bool sk) {
   static std::mutex mu;
-  static bool done[kMaxDev][5] = {};
+  static bool done[kMaxDev][5][2] = {};
   const int dev = current_device(), ti = tile_index(bn);
   std::lock_guard<std::mutex> lock(mu);
-  if (done[dev][ti]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_for(bn));
+  if (done[dev][ti][sk]) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel_for(bn, sk),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(bn, sk));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(trace_kernel_for(bn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem_for(bn));
-  if (e == cudaSuccess) done[dev][ti] = true;
+    e = cudaFuncSetAttribute(trace_kernel_for(bn, sk), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_for(bn, sk));
+  if (e == cudaSuccess) done[dev][ti][sk] = true;
   return e;
 }
 
 // How many clusters of S CTAs (or, for S == 1, CTAs) can be resident at once on this device.
 // Cluster placement is GPC-constrained, so this is not simply SMs * CTAs-per-SM / S.
-int max_resident(int bn, int S) {
+int max_resident(int bn, bool sk, int S) {
   static std::mutex mu;
-  static int cache[kMaxDev][5][quick::kMaxSplit + 1] = {};
+  static int cache[kMaxDev][5][2][quick::kMaxSplit + 1] = {};
   const int dev = current_device(), ti = tile_index(bn);
   {
     std::lock_guard<std::mutex> lock(mu);
-    if (cache[dev][ti][S]) return cache[dev][ti][S];
+    if (cache[dev][ti][sk][S]) return cache[dev][ti][sk][S];
   }
   int n = 0;
-  if (configure_kernel(bn) == cudaSuccess) {
+  if (configure_kernel(bn, sk) == cudaSuccess) {
     if (S == 1) {
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(bn), quick::kThreads,
-                                                        smem_for(bn)) == cudaSuccess)
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(bn, sk), quick::kThreads,
+                                                        smem_for(bn, sk)) == cudaSuccess)
         n = per_sm * sm_count();
     } else {
       cudaLaunchConfig_t cfg;
       std::memset(&cfg, 0, sizeof(cfg));
       cfg.gridDim = dim3((unsigned)S, 1, 1);
       cfg.blockDim = dim3(quick::kThreads, 1, 1);
-      cfg.dynamicSmemBytes = smem_for(bn);
+      cfg.dynamicSmemBytes = smem_for(bn, sk);
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeClusterDimension;
       attr.val.clusterDim.x = (unsigned)S;
@@ -766,98 +909,164 @@ int max_resident(int bn, int S) {
       attr.val.clusterDim.z = 1;
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&n, kernel_for(bn), &cfg) != cudaSuccess) n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kernel_for(bn, sk), &cfg) != cudaSuccess) n = 0;
     }
   }
   cudaGetLastError();  // occupancy queries must not leave a sticky error behind
   if (n <= 0) n = (S == 1 ? sm_count() : sm_count() / (2 * S));
   if (n <= 0) n = 1;
   std::lock_guard<std::mutex> lock(mu);
-  cache[dev][ti][S] = n;
+  cache[dev][ti][sk][S] = n;
   return n;
+}
+
+// ---------------------------------------------------------------------------------------
+// Stream-K workspace: per (device, stream), allocated on the first call outside graph
+// capture (partial tiles [P][2][BN][128] fp32 + one arrival counter per tile, zeroed once and
+// reset by the kernel).  A call under capture without a large-enough workspace uses the
+// cluster split-K plan instead, which needs none.
+struct Workspace {
+  int dev;
+  cudaStream_t stream;
+  float* ws;
+  size_t ws_bytes;
+  int* sems;
+  size_t n_sems;
+};
+
+bool get_workspace(cudaStream_t stream, size_t ws_bytes, size_t n_sems, float** ws, int** sems) {
+  static std::mutex mu;
+  static std::vector<Workspace> table;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  Workspace* w = nullptr;
+  for (auto& e : table)
+    if (e.dev == dev && e.stream == stream) w = &e;
+  if (w != nullptr && w->ws_bytes >= ws_bytes && w->n_sems >= n_sems) {
+    *ws = w->ws;
+    *sems = w->sems;
+    return true;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return false;
+  }
+  const size_t nb = std::max(ws_bytes, w ? w->ws_bytes : (size_t)0);
+  const size_t ns = std::max(n_sems, w ? w->n_sems : (size_t)0);
+  float* new_ws = nullptr;
+  int* new_sems = nullptr;
+  if (cudaMalloc(&new_ws, nb) != cudaSuccess || cudaMalloc(&new_sems, ns * sizeof(int)) != cudaSuccess ||
+      cudaMemsetAsync(new_sems, 0, ns * sizeof(int), stream) != cudaSuccess) {
+    cudaGetLastError();
+    if (new_ws) cudaFree(new_ws);
+    return false;
+  }
+  if (w != nullptr) {
+    // the old buffers may still be used by kernels queued on this stream: free stream-ordered
+    cudaStreamSynchronize(stream);
+    cudaFree(w->ws);
+    cudaFree(w->sems);
+    w->ws = new_ws;
+    w->sems = new_sems;
+    w->ws_bytes = nb;
+    w->n_sems = ns;
+  } else {
+    table.push_back(Workspace{dev, stream, new_ws, nb, new_sems, ns});
+  }
+  *ws = new_ws;
+  *sems = new_sems;
+  return true;
 }
 
 struct Plan {
   int tile_n, split, ctas;
+  bool sk;
+  int P;   // stream-K CTAs
 };
+
+constexpr int kMaxAccumK = 8192;
 
 // tile 256 (1 CTA/SM, 2-stage ring) measured slower than tile 128 at every M >= 128 on B200
 // (tools/tune_plan.py), so the automatic plan tiles large M by 128 tokens
-constexpr int kMaxAccumK = 8192;
-
 int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128; }
 
 // Launch plan (tuned with tools/tune_plan.py on B200):
 //  - tokens per tile: the smallest MMA N covering M, at most 128 (weights are dequantized once
 //    per m-tile; M > 128 tiles the tokens by 128);
-//  - split-K: the largest S <= 8 such that all tiles x S CTAs are resident in one wave (TMEM
-//    and shared memory allow 2 CTAs/SM up to tile 128, 1 above; clusters are GPC-placed, so
-//    residency is queried, not computed) and every CTA keeps >= 4 stages of K.
-Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split) {
+//  - tiles <= 64 (the HBM-bound regime): stream-K over (tile, 128-k stage) units with one wave
+//    of 2 CTAs per SM, each CTA a contiguous range of >= 4 units;
+//  - otherwise split-K over a cluster: the largest S <= 8 such that all tiles x S CTAs are
+//    resident in one wave (clusters are GPC-placed, so residency is queried) and every CTA
+//    keeps >= 2 A stages; then S >= ceil(K / 8192) for accuracy (a TMEM accumulator sums at
+//    most 8192 of K, R15).
+Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bool allow_sk) {
   (void)G;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
   const int tiles = (N / quick::kTileRows) * ((M + tn - 1) / tn);
+  if (allow_sk && force_split == 0 && sk_capable(tn)) {
+    const long long U = (long long)tiles * NA;
+    const long long resident = (long long)max_resident(tn, true, 1);
+    long long P = std::min(resident, std::max(1LL, U / 4));
+    // accuracy: a CTA's segment of one tile spans at most kMaxAccumK of K
+    const long long p_min = (U * quick::kKA + kMaxAccumK - 1) / kMaxAccumK;
+    if (P < p_min) P = std::min(resident, p_min);
+    if (U / P <= kMaxAccumK / quick::kKA) return Plan{tn, 1, (int)P, true, (int)P};
+  }
   int S = 1;
   if (force_split > 0) {
     S = force_split;
   } else {
-    const int per_sm = 512 / tmem_cols_for(tn);
+    const int per_sm = 512 / tmem_cols_for(tn, false);
     const int cap = per_sm * sm_count();
     for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= NA / 2; ++s2) {
       if (tiles * s2 > cap) break;
-      if (tiles > max_resident(tn, s2)) continue;
+      if (tiles > max_resident(tn, false, s2)) continue;
       S = s2;
     }
-    // accuracy: one TMEM fp32 accumulator sums at most kMaxAccumK of K (the tensor-core
-    // accumulation error grows with the summed length; at K = 28672 a single accumulator
-    // exceeds the 1e-2 relative bound near |y| = 1e-2)
     const int s_min = (K + kMaxAccumK - 1) / kMaxAccumK;
     if (S < s_min) S = std::min(s_min, quick::kMaxSplit);
   }
-  return Plan{tn, S, tiles * S};
+  return Plan{tn, S, tiles * S, false, 0};
 }
 
-template <int BN>
-quick_status_t launch_bn(const CUtensorMap& tmap, const void* packed, void* Y, int M, int N, int K,
-                         int G, int ldy, int flags, int S, cudaStream_t stream) {
-  using C = quick::Cfg<BN>;
-  cudaError_t e = configure_kernel(BN);
+template <int BN, bool SK>
+quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int P,
+                         cudaStream_t stream) {
+  using C = quick::Cfg<BN, SK>;
+  cudaError_t e = configure_kernel(BN, SK);
   if (e != cudaSuccess) return cuda_fail(e);
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)S, (unsigned)(N / quick::kTileRows), (unsigned)((M + BN - 1) / BN));
+  if (SK)
+    cfg.gridDim = dim3((unsigned)P, 1, 1);
+  else
+    cfg.gridDim = dim3((unsigned)S, (unsigned)kp.n_tiles, (unsigned)kp.m_tiles);
   cfg.blockDim = dim3(quick::kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  if (S > 1) {
+  if (!SK && S > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = (unsigned)S;
     attr[na].val.clusterDim.y = 1;
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (flags & QUICK_FLAG_PDL) {
+  if (kp.flags & QUICK_FLAG_PDL) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  int g_shift = -1;
-  if ((G & (G - 1)) == 0) {
-    g_shift = 0;
-    while ((1 << g_shift) < G) ++g_shift;
-  }
-  const uint8_t* pk = static_cast<const uint8_t*>(packed);
+  kp.trace = g_trace;
   if (g_trace != nullptr)
-    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, true>, tmap, pk, Y, M, N, K, G,
-                           g_shift, ldy, flags, g_trace);
+    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true>, tmap, kp);
   else
-    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, false>, tmap, pk, Y, M, N, K, G,
-                           g_shift, ldy, flags, (unsigned long long*)nullptr);
+    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false>, tmap, kp);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
 }
@@ -870,8 +1079,9 @@ extern "C" {
 
 int quick_last_cuda_error(void) { return g_last_cuda_error; }
 
-// Debug only (not part of quick.h): device buffer of 16 * (8 + 7 * 256) uint64 clock stamps
-// written by the next launches for CTAs with blockIdx.z == 0 and blockIdx.y < 2; NULL disables.
+// Debug only (not part of quick.h): device buffer of 16 * (8 + 7 * 256) + 3 * CTAs uint64 stamps
+// written by the next launches (detailed per-stage stamps for 16 CTAs, start/end for all CTAs);
+// NULL disables.
 void quick_debug_set_trace(void* device_buffer) {
   g_trace = static_cast<unsigned long long*>(device_buffer);
 }
@@ -880,9 +1090,9 @@ quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* spl
                                int* num_ctas) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
-  const Plan p = choose_plan(M > 0 ? M : 1, N, K, G, 0, 0);
+  const Plan p = choose_plan(M > 0 ? M : 1, N, K, G, 0, 0, true);
   if (tile_n) *tile_n = p.tile_n;
-  if (split_k) *split_k = p.split;
+  if (split_k) *split_k = p.sk ? 0 : p.split;   // 0 = stream-K
   if (num_ctas) *num_ctas = p.ctas;
   return QUICK_OK;
 }
@@ -895,14 +1105,30 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (M == 0) return QUICK_OK;
   if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
-  if (ldy % 8 != 0 || (flags & ~(QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL)) != 0)
-    return QUICK_ERR_UNSUPPORTED;
+  const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK;
+  if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   if (split_k < 0 || split_k > quick::kMaxSplit || split_k > NA) return QUICK_ERR_UNSUPPORTED;
 
-  const Plan plan = choose_plan(M, N, K, G, tile_n, split_k);
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  Plan plan = choose_plan(M, N, K, G, tile_n, split_k, (flags & QUICK_FLAG_NO_STREAMK) == 0);
+  quick::KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.n_tiles = N / quick::kTileRows;
+  kp.m_tiles = (M + plan.tile_n - 1) / plan.tile_n;
+  if (plan.sk) {
+    float* ws = nullptr;
+    int* sems = nullptr;
+    const size_t ws_bytes = (size_t)plan.P * 2 * plan.tile_n * quick::kTileRows * sizeof(float);
+    if (get_workspace(strm, ws_bytes, (size_t)kp.n_tiles * kp.m_tiles, &ws, &sems)) {
+      kp.ws = ws;
+      kp.sems = sems;
+    } else {
+      plan = choose_plan(M, N, K, G, tile_n, split_k, false);   // no workspace (graph capture)
+    }
+  }
   const int tn = plan.tile_n, s = plan.split;
 
   EncodeTiledFn enc = get_encode_fn();
@@ -910,7 +1136,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   // X viewed as [K/64][M][64] (dims innermost first: k within a 64-chunk, token, k-chunk): one
   // 3-D box {64, tile_n, KL/64} lands as KL/64 SWIZZLE_128B [tile_n][64] sub-tiles.
   CUtensorMap tmap;
-  const int kl = kl_for(tn);
+  const int kl = kl_for(tn, plan.sk);
   cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
   cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
   cuuint32_t box[3] = {64, (cuuint32_t)tn, (cuuint32_t)(kl / 64)};
@@ -920,13 +1146,35 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
 
-  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  kp.packed = static_cast<const uint8_t*>(packed);
+  kp.Y = Y;
+  kp.M = M;
+  kp.N = N;
+  kp.K = K;
+  kp.G = G;
+  kp.g_shift = -1;
+  if ((G & (G - 1)) == 0) {
+    kp.g_shift = 0;
+    while ((1 << kp.g_shift) < G) ++kp.g_shift;
+  }
+  kp.ldy = ldy;
+  kp.flags = flags;
+  kp.NA = NA;
+  kp.U = (long long)kp.n_tiles * kp.m_tiles * NA;
+  kp.P = plan.P;
+  if (plan.sk) {
+    switch (tn) {
+      case 16: return launch_bn<16, true>(tmap, kp, 1, plan.P, strm);
+      case 32: return launch_bn<32, true>(tmap, kp, 1, plan.P, strm);
+      default: return launch_bn<64, true>(tmap, kp, 1, plan.P, strm);
+    }
+  }
   switch (tn) {
-    case 16: return launch_bn<16>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    case 32: return launch_bn<32>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    case 64: return launch_bn<64>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    case 128: return launch_bn<128>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
-    default: return launch_bn<256>(tmap, packed, Y, M, N, K, G, ldy, flags, s, strm);
+    case 16: return launch_bn<16, false>(tmap, kp, s, 0, strm);
+    case 32: return launch_bn<32, false>(tmap, kp, s, 0, strm);
+    case 64: return launch_bn<64, false>(tmap, kp, s, 0, strm);
+    case 128: return launch_bn<128, false>(tmap, kp, s, 0, strm);
+    default: return launch_bn<256, false>(tmap, kp, s, 0, strm);
   }
 }
 

@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libquick.so")
 
 QUICK_OK, QUICK_ERR_INVALID_ARG, QUICK_ERR_UNSUPPORTED, QUICK_ERR_CUDA = 0, 1, 2, 3
-QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL = 1, 2
+QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL, QUICK_FLAG_NO_STREAMK = 1, 2, 4
 
 
 class QuickError(RuntimeError):
@@ -116,7 +116,7 @@ def quick_gemm_plan(M: int, N: int, K: int, group_size: int):
 
 # ----------------------------------------------------------------------------- device side
 def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ldy=None, out_fp32=False,
-                     pdl=False, tile_n: int = 0, split_k: int = 0, stream=None):
+                     pdl=False, no_streamk=False, tile_n: int = 0, split_k: int = 0, stream=None):
     """Y = X . dequant(Wq) on the GPU.  x: cuda fp16 [M][K]; packed: cuda uint8 blob.
     Returns `out` (allocated if None): fp16 [M][N] (fp32 if out_fp32)."""
     import torch
@@ -128,7 +128,8 @@ def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ld
     ld = out.stride(0) if ldy is None else ldy
     _check("quick_w4a16_gemm_ex", _lib.quick_w4a16_gemm_ex(
         ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(packed.data_ptr()), M, N, K, group_size,
-        ctypes.c_void_p(out.data_ptr()), ld, (QUICK_FLAG_OUT_F32 if out_fp32 else 0) | (QUICK_FLAG_PDL if pdl else 0),
+        ctypes.c_void_p(out.data_ptr()), ld, (QUICK_FLAG_OUT_F32 if out_fp32 else 0) | (QUICK_FLAG_PDL if pdl else 0)
+        | (QUICK_FLAG_NO_STREAMK if no_streamk else 0),
         tile_n, split_k, _stream_handle(stream)))
     return out
 

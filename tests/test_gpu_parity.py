@@ -126,6 +126,7 @@ def test_group_sizes(G):
     if p.K % G:
         pytest.skip("K not a multiple of G")
     check_tol(p, run(p))
+    check_tol(p, run(p, no_streamk=True))
     check_tol(p, run(p, split_k=3))
     check_tol(p, run(p, tile_n=128))
 
@@ -135,6 +136,34 @@ def test_llama7b_attention_sweep(M):
     """BASELINE.json configs[1]: N = K = 4096, g128, full-output parity."""
     p = synth.make_problem(100 + M, M=M, N=4096, K=4096, G=128)
     check_tol(p, run(p), M)
+
+
+@pytest.mark.parametrize("M,N,K,G", [(1, 512, 1024, 128), (7, 384, 1152, 128), (16, 256, 1088, 64),
+                                     (33, 640, 2048, 128), (64, 1024, 4224, 32), (3, 128, 256, 128),
+                                     (9, 4096, 4096, 128), (16, 28672, 1024, 128)])
+def test_stream_k_segments(M, N, K, G):
+    """Stream-K (auto plan, tiles <= 64): CTAs own unit ranges that cross tile boundaries;
+    partial tiles are summed by the last CTA in fixed order -- vs the oracle, vs the cluster
+    split-K plan, and run-to-run bit-identical.  Shapes include odd A-stage counts and a
+    64-k ragged tail (K % 128 == 64)."""
+    p = synth.make_problem(M * 7 + K, M=M, N=N, K=K, G=G)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    plan = quick.quick_gemm_plan(M, N, K, G)
+    y1 = quick.quick_w4a16_gemm(x, blob, N, K, G)
+    y2 = quick.quick_w4a16_gemm(x, blob, N, K, G)
+    yc = quick.quick_w4a16_gemm(x, blob, N, K, G, no_streamk=True)
+    torch.cuda.synchronize()
+    check_tol(p, y1, plan)
+    check_tol(p, yc, "cluster")
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+
+
+def test_stream_k_exact_sets():
+    for kind in ("intexact", "onehot"):
+        p = synth.make_structured(kind, 8, M=16, N=1024, K=2048, G=128)
+        y = run(p)
+        ref = oracle.round_fp16(oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128))
+        np.testing.assert_array_equal(f16_bits(y), ref.view(np.uint16))
 
 
 def test_fp32_output_and_ldy():
