@@ -1086,6 +1086,18 @@ void quick_debug_set_trace(void* device_buffer) {
   g_trace = static_cast<unsigned long long*>(device_buffer);
 }
 
+// Debug only: resident CTAs (S == 1) or clusters (S > 1) of the (tile, stream-K) kernel, and
+// its dynamic shared memory bytes.
+int quick_debug_resident(int bn, int sk, int S, int* smem_bytes, int* regs) {
+  if (tile_index(bn) < 0 || S < 1 || S > quick::kMaxSplit || (sk && !sk_capable(bn))) return -1;
+  if (smem_bytes) *smem_bytes = smem_for(bn, sk != 0);
+  if (regs) {
+    cudaFuncAttributes fa;
+    *regs = cudaFuncGetAttributes(&fa, kernel_for(bn, sk != 0)) == cudaSuccess ? fa.numRegs : -1;
+  }
+  return max_resident(bn, sk != 0, S);
+}
+
 quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* split_k,
                                int* num_ctas) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
