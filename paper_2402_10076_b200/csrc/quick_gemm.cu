@@ -875,6 +875,14 @@ cudaError_t configure_kernel(int bn, bool sk) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(trace_kernel_for(bn, sk), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem_for(bn, sk));
+  // the whole unified L1/shared array as shared memory: two 80-110 KiB CTAs per SM (without
+  // this the occupancy calculator, and the launch, may assume a smaller carveout and one CTA)
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kernel_for(bn, sk), cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(trace_kernel_for(bn, sk), cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
   if (e == cudaSuccess) done[dev][ti][sk] = true;
   return e;
 }
