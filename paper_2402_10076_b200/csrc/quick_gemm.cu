@@ -900,10 +900,16 @@ int max_resident(int bn, bool sk, int S) {
   int n = 0;
   if (configure_kernel(bn, sk) == cudaSuccess) {
     if (S == 1) {
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for(bn, sk), quick::kThreads,
-                                                        smem_for(bn, sk)) == cudaSuccess)
-        n = per_sm * sm_count();
+      // per-SM limits computed directly: TMEM columns, shared memory (228 KiB per SM, 1 KiB
+      // reserved per CTA), registers (64 K).  (cudaOccupancyMaxActiveBlocksPerMultiprocessor
+      // reports 1 here although the hardware co-schedules 2 -- observed with %smid traces.)
+      cudaFuncAttributes fa;
+      int regs = 96;
+      if (cudaFuncGetAttributes(&fa, kernel_for(bn, sk)) == cudaSuccess) regs = fa.numRegs;
+      const int by_tmem = 512 / tmem_cols_for(bn, sk);
+      const int by_smem = (228 * 1024) / (smem_for(bn, sk) + 1024);
+      const int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * (quick::kThreads / 32));
+      n = std::max(1, std::min(by_tmem, std::min(by_smem, by_regs))) * sm_count();
     } else {
       cudaLaunchConfig_t cfg;
       std::memset(&cfg, 0, sizeof(cfg));
