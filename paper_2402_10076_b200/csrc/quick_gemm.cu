@@ -49,6 +49,7 @@ constexpr int kMetaBytes = 320;   // 128 fp16 scales + 128 4-bit zeros per (n-ti
 constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable clusters)
 constexpr int kTraceStages = 256; // debug tracing: stages recorded per traced CTA
 constexpr int kTraceStride = 8 + 7 * kTraceStages;
+constexpr int kDebugNoCompute = 1 << 30;   // undocumented debug flag: stream the loads only
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
   const int NG = K / G;
   const bool out_fp32 = (p.flags & QUICK_FLAG_OUT_F32) != 0;
   const bool pdl = (p.flags & QUICK_FLAG_PDL) != 0;
+  const bool dbg_nocompute = (p.flags & kDebugNoCompute) != 0;   // load path only (debug)
   const int g_shift = p.g_shift;
   // group index of k: shift when G is a power of two, division otherwise
   auto group_of = [&](int k) { return g_shift >= 0 ? (k >> g_shift) : (k / G); };
@@ -392,6 +394,11 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         const int kv = min(kKA, K - a * kKA);   // 128, or 64 at the end of K
         const bool last_of_load = (sub == APL - 1) || (a == sg.a_hi - 1);
         if (ptx::elect_one()) {
+          if (dbg_nocompute) {
+            ptx::mma_commit(bar_aempty + 8 * as);
+            if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);
+            if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
+          } else {
           const uint32_t a_col = tmem + as * kAColsPerStage;
           // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
           const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES + sub * 2 * C::X_SUB) >> 4);
@@ -406,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
           ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
           if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage used
           if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);  // segment accumulated
+          }
         }
         __syncwarp();
         if (lane == 0) stamp(6, ia);
@@ -496,6 +504,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         // segment) gets the other parity's share from the same thread
         const int in_load = min(APL, sg.a_hi - (a - sub));
         ptx::mbar_arrive_cnt(bar_empty + 8 * slot, (uint32_t)(APL - in_load + 1));
+        if (dbg_nocompute) {
+          const int as0 = ia % kAStages;
+          ptx::mbar_wait(bar_aempty + 8 * as0, (uint32_t)(((ia / kAStages) & 1) ^ 1));
+          ptx::mbar_arrive(bar_afull + 8 * as0);
+          continue;
+        }
         const int as = ia % kAStages;
         const uint32_t aph = (uint32_t)((ia / kAStages) & 1);
         dequant_word(w[0].x, cst, a_regs + 0);
@@ -1131,7 +1145,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (M == 0) return QUICK_OK;
   if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
-  const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK;
+  const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
