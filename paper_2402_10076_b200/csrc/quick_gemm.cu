@@ -603,6 +603,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
           for (int i = 0; i < 8; ++i)
             if (jc + i < jmax) __stcg(slot_ws + (jc + i) * kTileRows + r, __uint_as_float(v[i]));
         }
+        // the accumulator has been read: let the MMA reuse it before the cross-CTA fix-up
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar_dempty + 8 * db);
         const long long u_first = (long long)sg.tile * p.NA;
         const int c_first = sk_cta_of(u_first, p.U, p.P);
         const int c_last = sk_cta_of(u_first + p.NA - 1, p.U, p.P);
@@ -614,24 +617,53 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         }
         ptx::named_bar_sync(1, kDqThreads);
         if (*sk_flag) {
+          // last arriver: sum the partials of CTAs c_first..c_last in that order (deterministic),
+          // the tile spread over the 256 dequant threads as float4 columns-of-rows, with up to
+          // 8 partial loads in flight before the in-order adds
           __threadfence();
-#pragma unroll 1
-          for (int jc = j0; jc < jmax; ++jc) {
-            float acc = 0.f;
-            for (int c = c_first; c <= c_last; ++c) {
-              const int sl = (sk_start(c, p.U, p.P) >= u_first) ? 0 : 1;
-              acc += __ldcg(p.ws + ((size_t)c * 2 + sl) * (BN * kTileRows) + jc * kTileRows + r);
+          const int jvalid = min(BN, M - m0);
+          const int tid = (int)threadIdx.x - 64;
+          for (int e4 = tid; e4 < jvalid * (kTileRows / 4); e4 += kDqThreads) {
+            const int j = e4 / (kTileRows / 4);
+            const int r4 = (e4 % (kTileRows / 4)) * 4;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int c0 = c_first; c0 <= c_last; c0 += 8) {
+              float4 v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int c = c0 + u;
+                if (c <= c_last) {
+                  const int sl = (sk_start(c, p.U, p.P) >= u_first) ? 0 : 1;
+                  v[u] = __ldcg(reinterpret_cast<const float4*>(
+                      p.ws + ((size_t)c * 2 + sl) * (BN * kTileRows) + j * kTileRows + r4));
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                if (c0 + u <= c_last) {
+                  acc.x += v[u].x;
+                  acc.y += v[u].y;
+                  acc.z += v[u].z;
+                  acc.w += v[u].w;
+                }
+              }
             }
-            const int m = m0 + jc;
-            if (out_fp32)
-              reinterpret_cast<float*>(p.Y)[(size_t)m * p.ldy + n] = acc;
-            else
-              reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(acc);
+            const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)sg.t * kTileRows + r4;
+            if (out_fp32) {
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
+            } else {
+              __half2 lo = __floats2half2_rn(acc.x, acc.y);
+              __half2 hi = __floats2half2_rn(acc.z, acc.w);
+              uint2 pk;
+              pk.x = *reinterpret_cast<uint32_t*>(&lo);
+              pk.y = *reinterpret_cast<uint32_t*>(&hi);
+              *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
+            }
           }
           if (threadIdx.x == 64) p.sems[sg.tile] = 0;   // self-reset for the next launch
         }
       }
-      if (SK) {
+      if (SK && whole) {
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar_dempty + 8 * db);
       }

@@ -47,6 +47,12 @@ if len(rec):
     print(f"ALL CTAs: {len(rec)} on {len(per_sm)} SMs, CTAs/SM histogram {cnt.tolist()}, kernel span {span:.2f} us, "
           f"CTA duration min/med/max {dur.min():.2f}/{np.median(dur):.2f}/{dur.max():.2f} us, SM finish min/med/max "
           f"{busy.min():.2f}/{np.median(busy):.2f}/{busy.max():.2f} us, start skew max {(rec[:,1].max()-t0)/1e3:.2f} us")
+    full = tt[16 * STRIDE:].reshape(-1, 3)
+    idx = np.nonzero(full[:, 1] > 0)[0]
+    d_all = (full[idx, 2] - full[idx, 1]) / 1e3
+    slow = idx[d_all > 2 * np.median(d_all)]
+    print("slow CTAs (lin idx, smid, start us, dur us):",
+          [(int(i), int(full[i, 0]), round((full[i, 1] - t0) / 1e3, 2), round((full[i, 2] - full[i, 1]) / 1e3, 2)) for i in slow[:20]])
 print("plan", quick.quick_gemm_plan(M, N, K, G), "tile", tn, "split", sk)
 names = ["P_before_empty", "P_issued", "D_full", "D_aempty_ok", "D_afull_arrived", "M_afull_ok", "M_committed"]
 for c in range(16):
