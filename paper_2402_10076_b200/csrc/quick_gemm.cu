@@ -66,7 +66,7 @@ struct Cfg {
   static constexpr int DCOL = ASTAGES * kAColsPerStage;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
-  static constexpr int STAGES = BN <= 16 ? 3 : BN <= 32 ? 3 : BN <= 64 ? 4 : 2;
+  static constexpr int STAGES = BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 64 ? 4 : 2;
   static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
@@ -245,7 +245,7 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
 }
 
-template <int BN, bool SK, bool TRACE>
+template <int BN, bool SK, bool GBIG, bool TRACE>
 __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const __grid_constant__ KParams p) {
@@ -454,7 +454,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
       return make_consts(ptx::lds_u16(mrow + mo), (ptx::lds_u8(zrow + mo) >> zsh) & 0xFu);
     };
     const bool tw = TRACE && (warp == 2 && lane == 0);
-    const bool g_big = (G % kKA) == 0;    // a group spans whole A stages
     constexpr int kColsPerWarp = BN / 2;
     const int j0 = par * kColsPerWarp;   // this warp's half of the accumulator columns
     uint32_t a_regs[32];
@@ -488,15 +487,14 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
           w[2] = make_uint4(0, 0, 0, 0);
           w[3] = w[2];
         }
-        if (g_big) {
+        DequantConsts cst1;
+        if constexpr (GBIG) {
           const int g = group_of(ka);
           if (g != g_prev) {
             cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
             g_prev = g;
           }
-        }
-        DequantConsts cst1 = cst;
-        if (!g_big) {
+        } else {
           cst = consts_at(moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes);
           cst1 = consts_at(moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes);
         }
@@ -516,30 +514,33 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         dequant_word(w[0].y, cst, a_regs + 4);
         dequant_word(w[0].z, cst, a_regs + 8);
         dequant_word(w[0].w, cst, a_regs + 12);
-        dequant_word(w[1].x, cst1, a_regs + 16);
-        dequant_word(w[1].y, cst1, a_regs + 20);
-        dequant_word(w[1].z, cst1, a_regs + 24);
-        dequant_word(w[1].w, cst1, a_regs + 28);
+        const DequantConsts& c1 = GBIG ? cst : cst1;
+        dequant_word(w[1].x, c1, a_regs + 16);
+        dequant_word(w[1].y, c1, a_regs + 20);
+        dequant_word(w[1].z, c1, a_regs + 24);
+        dequant_word(w[1].w, c1, a_regs + 28);
         ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
         if (tw) stamp(3, ia);
         ptx::tc_fence_after();
         const uint32_t acol = tmem + tlane + as * kAColsPerStage;
         ptx::tmem_st_32x32b_x32(acol, a_regs);
         if (full_stage) {
-          DequantConsts cst2 = cst, cst3 = cst;
-          if (!g_big) {
+          DequantConsts cst2, cst3;
+          if constexpr (!GBIG) {
             cst2 = consts_at(moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes);
             cst3 = consts_at(moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes);
           }
+          const DequantConsts& c2 = GBIG ? cst : cst2;
+          const DequantConsts& c3 = GBIG ? cst : cst3;
           uint32_t b_regs[32];
-          dequant_word(w[2].x, cst2, b_regs + 0);
-          dequant_word(w[2].y, cst2, b_regs + 4);
-          dequant_word(w[2].z, cst2, b_regs + 8);
-          dequant_word(w[2].w, cst2, b_regs + 12);
-          dequant_word(w[3].x, cst3, b_regs + 16);
-          dequant_word(w[3].y, cst3, b_regs + 20);
-          dequant_word(w[3].z, cst3, b_regs + 24);
-          dequant_word(w[3].w, cst3, b_regs + 28);
+          dequant_word(w[2].x, c2, b_regs + 0);
+          dequant_word(w[2].y, c2, b_regs + 4);
+          dequant_word(w[2].z, c2, b_regs + 8);
+          dequant_word(w[2].w, c2, b_regs + 12);
+          dequant_word(w[3].x, c3, b_regs + 16);
+          dequant_word(w[3].y, c3, b_regs + 20);
+          dequant_word(w[3].z, c3, b_regs + 24);
+          dequant_word(w[3].w, c3, b_regs + 28);
           ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
         }
         ptx::tmem_wait_st();
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         if (*sk_flag) {
           // last arriver: sum the partials of CTAs c_first..c_last in that order (deterministic),
           // the tile spread over the 256 dequant threads as float4 columns-of-rows, with up to
-          // 8 partial loads in flight before the in-order adds
+          // 4 partial loads in flight before the in-order adds
           __threadfence();
           const int jvalid = min(BN, M - m0);
           const int tid = (int)threadIdx.x - 64;
@@ -627,10 +628,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
             const int j = e4 / (kTileRows / 4);
             const int r4 = (e4 % (kTileRows / 4)) * 4;
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int c0 = c_first; c0 <= c_last; c0 += 8) {
-              float4 v[8];
+            for (int c0 = c_first; c0 <= c_last; c0 += 4) {
+              float4 v[4];
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
+              for (int u = 0; u < 4; ++u) {
                 const int c = c0 + u;
                 if (c <= c_last) {
                   const int sl = (sk_start(c, p.U, p.P) >= u_first) ? 0 : 1;
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
                 }
               }
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
+              for (int u = 0; u < 4; ++u) {
                 if (c0 + u <= c_last) {
                   acc.x += v[u].x;
                   acc.y += v[u].y;
@@ -878,21 +879,22 @@ quick_status_t check_gemm_shape(int M, int N, int K, int G) {
 inline bool sk_capable(int bn) { return bn <= 64; }
 
 template <int BN, bool SK, bool TRACE>
-void* kernel_ptr() {
-  return reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, SK, TRACE>);
+void* kernel_ptr2(bool gbig) {
+  return gbig ? reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, SK, true, TRACE>)
+              : reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, SK, false, TRACE>);
 }
 template <bool TRACE>
-void* kernel_for_t(int bn, bool sk) {
+void* kernel_for_t(int bn, bool sk, bool gbig) {
   switch (bn) {
-    case 16: return sk ? kernel_ptr<16, true, TRACE>() : kernel_ptr<16, false, TRACE>();
-    case 32: return sk ? kernel_ptr<32, true, TRACE>() : kernel_ptr<32, false, TRACE>();
-    case 64: return sk ? kernel_ptr<64, true, TRACE>() : kernel_ptr<64, false, TRACE>();
-    case 128: return kernel_ptr<128, false, TRACE>();
-    default: return kernel_ptr<256, false, TRACE>();
+    case 16: return sk ? kernel_ptr2<16, true, TRACE>(gbig) : kernel_ptr2<16, false, TRACE>(gbig);
+    case 32: return sk ? kernel_ptr2<32, true, TRACE>(gbig) : kernel_ptr2<32, false, TRACE>(gbig);
+    case 64: return sk ? kernel_ptr2<64, true, TRACE>(gbig) : kernel_ptr2<64, false, TRACE>(gbig);
+    case 128: return kernel_ptr2<128, false, TRACE>(gbig);
+    default: return kernel_ptr2<256, false, TRACE>(gbig);
   }
 }
-void* kernel_for(int bn, bool sk) { return kernel_for_t<false>(bn, sk); }
-void* trace_kernel_for(int bn, bool sk) { return kernel_for_t<true>(bn, sk); }
+void* kernel_for(int bn, bool sk, bool gbig = true) { return kernel_for_t<false>(bn, sk, gbig); }
+void* trace_kernel_for(int bn, bool sk, bool gbig = true) { return kernel_for_t<true>(bn, sk, gbig); }
 
 #define QUICK_CFG_FIELD(FN, FIELD)                                                        \
   int FN(int bn, bool sk) {                                                               \
@@ -916,19 +918,16 @@ cudaError_t configure_kernel(int bn, bool sk) {
   const int dev = current_device(), ti = tile_index(bn);
   std::lock_guard<std::mutex> lock(mu);
   if (done[dev][ti][sk]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel_for(bn, sk),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(bn, sk));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(trace_kernel_for(bn, sk), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem_for(bn, sk));
-  // the whole unified L1/shared array as shared memory: two 80-110 KiB CTAs per SM (without
-  // this the occupancy calculator, and the launch, may assume a smaller carveout and one CTA)
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(kernel_for(bn, sk), cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(trace_kernel_for(bn, sk), cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
+  cudaError_t e = cudaSuccess;
+  // every (group-size specialisation, trace) variant; the whole unified L1/shared array as
+  // shared memory: two 80-110 KiB CTAs per SM
+  for (int v = 0; v < 4 && e == cudaSuccess; ++v) {
+    void* k = (v & 2) ? trace_kernel_for(bn, sk, v & 1) : kernel_for(bn, sk, v & 1);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(bn, sk));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               (int)cudaSharedmemCarveoutMaxShared);
+  }
   if (e == cudaSuccess) done[dev][ti][sk] = true;
   return e;
 }
@@ -1123,10 +1122,13 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   cfg.attrs = attr;
   cfg.numAttrs = na;
   kp.trace = g_trace;
+  const bool gbig = (kp.G % quick::kKA) == 0;
   if (g_trace != nullptr)
-    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true>, tmap, kp);
+    e = gbig ? cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true, true>, tmap, kp)
+             : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, true>, tmap, kp);
   else
-    e = cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false>, tmap, kp);
+    e = gbig ? cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true, false>, tmap, kp)
+             : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, false>, tmap, kp);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
 }
