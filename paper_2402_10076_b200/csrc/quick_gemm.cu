@@ -66,7 +66,9 @@ struct Cfg {
   static constexpr int DCOL = ASTAGES * kAColsPerStage;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
-  static constexpr int STAGES = BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 64 ? 4 : 2;
+  // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
+  // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
+  static constexpr int STAGES = BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 64 ? 4 : BN <= 128 ? 4 : 2;
   static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
@@ -1077,8 +1079,7 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
   if (force_split > 0) {
     S = force_split;
   } else {
-    const int per_sm = 512 / tmem_cols_for(tn, false);
-    const int cap = per_sm * sm_count();
+    const int cap = max_resident(tn, false, 1);   // CTAs/SM from TMEM, smem and registers
     for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= NA / 2; ++s2) {
       if (tiles * s2 > cap) break;
       if (tiles > max_resident(tn, false, s2)) continue;
