@@ -11,17 +11,17 @@
 // with the weight rows n on the 128-lane MMA M dimension and the tokens m on the MMA N
 // dimension (16..256), so small batches do not waste the 128-row MMA.
 //
-// CTA = 10 warps, warp-specialised:
-//   warp 0      producer: TMA 2-D load of the X tile [BN tokens][64 k] (SWIZZLE_128B) and
-//               1-D bulk copies of the packed int4 stage (4 KiB) + group metadata into a
-//               STAGES-deep mbarrier ring
-//   warp 1      TMEM allocator + MMA issuer (one thread): 4 x tcgen05.mma.kind::f16 per
-//               64-k stage, fp32 accumulation in TMEM (reading R4), tcgen05.commit -> mbarriers
-//   warps 2..9  dequantizers, two groups of 4 taking alternate stages: per stage a thread
-//               (one TMEM lane = one weight row) does 2 x LDS.128 of 64 codes -> 8 x (LOP3 x4,
-//               HSUB2/HFMA2 -> exact (q-z), HMUL2 by s) -> tcgen05.st.32x32b.x32 into the TMEM
-//               A ring (software-pipelined against the next stage); then the epilogue (tcgen05.ld -> fp16/fp32 -> Y), or for split-K the fp32
-//               partial -> SMEM, cluster barrier, fixed-order DSMEM reduction (deterministic).
+// CTA = 10 warps, warp-specialised.  The SM's warp scheduler favours the highest
+// warp id, so the two latency-critical single warps take the top ids:
+//   warps 0..7  dequantizers, two groups of 4 taking alternate 128-k A stages: per stage a
+//               thread (one TMEM lane = one weight row) does 4 x LDS.128 of 128 codes ->
+//               16 x (SHF + LOP3 x4, HSUB2/HFMA2 -> exact (q-z), HMUL2 by s) -> 2 x
+//               tcgen05.st.32x32b.x32 into the TMEM A ring; then the segment epilogue
+//               (tcgen05.ld -> Y, or an fp32 partial for split-K / stream-K)
+//   warp 8      producer: 1-D bulk copies of the packed int4 stage + group metadata and a 3-D
+//               TMA load of the X tile (SWIZZLE_128B, K-major) into a STAGES-deep mbarrier ring
+//   warp 9      TMEM allocator + MMA issuer (one elected thread): 8 x tcgen05.mma.kind::f16
+//               per A stage, fp32 accumulation in TMEM, tcgen05.commit -> mbarriers
 // Split-K: the S CTAs of a (S,1,1) cluster share one (n-tile, m-tile) and split K (the
 // "split-k" knob of §5); partial sums stay fp32 (tolerance analysis).
 #include <cuda.h>
@@ -39,7 +39,9 @@
 
 namespace quick {
 
-constexpr int kThreads = 320;     // 10 warps: producer, MMA, 8 dequantizers (2 per TMEM lane quarter)
+constexpr int kThreads = 320;     // 10 warps: 8 dequantizers (2 per TMEM lane quarter), producer, MMA
+constexpr int kProducerWarp = 8;
+constexpr int kMmaWarp = 9;
 constexpr int kDqThreads = 256;   // the 8 dequantizer warps (named barrier 1 in stream-K epilogues)
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
@@ -50,20 +52,27 @@ constexpr int kMaxSplit = 8;      // split-K cluster size limit (portable cluste
 constexpr int kTraceStages = 256; // debug tracing: stages recorded per traced CTA
 constexpr int kTraceStride = 8 + 7 * kTraceStages;
 constexpr int kDebugNoCompute = 1 << 30;   // undocumented debug flag: stream the loads only
+constexpr int kDebugExitTop = 1 << 29;     // debug: return at kernel entry (launch cost probe)
+constexpr int kDebugExitPrologue = 1 << 28;  // debug: return after the prologue (setup probe)
+constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (commits only)
+constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
 //          metadata, one 3-D TMA of the [KL/64][BN][64] X tile (few, large async copies: each
 //          TMA/bulk issue costs ~150 SM cycles on B200, measured with tools/trace_gemm.py)
 //   STAGES depth of the load ring
-//   TMEM   A ring of ASTAGES x 64 columns, then NDBUF fp32 accumulators of BN columns (stream-K
-//          double-buffers D so a segment's epilogue overlaps the next segment's MMAs)
+//   TMEM   A ring of ASTAGES x 64 columns, then NDBUF x NACC fp32 accumulators of BN columns
+//          (stream-K double-buffers D so a segment's epilogue overlaps the next segment's MMAs;
+//          small tiles alternate the K=16 MMAs over NACC = 2 accumulators, summed in the
+//          epilogue, because a single accumulator chain makes N=16 MMAs latency-bound)
 template <int BN, bool SK>
 struct Cfg {
   static constexpr int NDBUF = SK ? 2 : 1;
   static constexpr int ASTAGES =
       BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2);
   static constexpr int DCOL = ASTAGES * kAColsPerStage;
+  static constexpr int NACC = (BN <= 32 && DCOL + NDBUF * 2 * BN <= 256) ? 2 : 1;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
@@ -81,7 +90,7 @@ struct Cfg {
   static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 4;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;   // TMEM base, then stream-K flag
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = (DCOL + NDBUF * BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512;
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
   static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
@@ -90,7 +99,7 @@ struct Cfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
   static_assert(KL % kKA == 0 && APL <= 2, "load stage = one or two A stages");
   static_assert(!SK || BN <= 64, "stream-K is used for the small-M tiles");
-  static_assert(DCOL + NDBUF * BN <= TMEM_COLS, "TMEM budget");
+  static_assert(DCOL + NDBUF * NACC * BN <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // split-K partial tile [BN][128] fp32 reuses the pipeline buffers once the mainloop is done
   static_assert(BN * kTileRows * 4 <= BAR_OFF, "split-K partial must fit in the pipeline smem");
@@ -103,10 +112,11 @@ struct KParams {
   int M, N, K, G, g_shift, ldy, flags;
   int n_tiles, m_tiles;   // tile index = t * m_tiles + mt (n-tile major: a CTA's tiles share weights)
   int NA;                 // A stages (128 k) per tile: ceil(K / 128)
-  // stream-K (gridDim = (P, 1, 1)): CTA c owns units [c U / P, (c+1) U / P) of the U = tiles x NA
-  // (tile, A stage) units; partial tiles go through ws and are summed by the last arriver
-  long long U;
-  int P;
+  // stream-K (gridDim = (P, 1, 1)): the U = tiles x NA (tile, A stage) units are cut into P
+  // contiguous ranges, U = P q + r: CTA c owns [c q + min(c, r), ...) of q + (c < r) units
+  // (32-bit, no division on the device); partial tiles go through ws and are summed by the
+  // last arriver
+  int U, P, sk_q, sk_r;
   float* ws;              // [P][2][BN][128] fp32 partial tiles (slot 0: first segment, 1: last)
   int* sems;              // [tiles] arrival counters, zero between launches (self-resetting)
   unsigned long long* trace;
@@ -120,7 +130,7 @@ struct Seg {
 // Enumerates this CTA's segments.  Cluster split-K: exactly one (blockIdx.y, blockIdx.z, the
 // split's A range).  Stream-K: the unit range of CTA blockIdx.x, cut at tile boundaries.
 struct SegIter {
-  long long u, u1;
+  int u, u1;
   int NA, m_tiles;
   bool sk, done;
   int t, mt, a_lo, a_hi;
@@ -130,8 +140,9 @@ struct SegIter {
     m_tiles = p.m_tiles;
     done = false;
     if (sk) {
-      u = ((long long)blockIdx.x * p.U) / p.P;
-      u1 = ((long long)(blockIdx.x + 1) * p.U) / p.P;
+      const int c = (int)blockIdx.x;
+      u = c * p.sk_q + min(c, p.sk_r);
+      u1 = u + p.sk_q + (c < p.sk_r ? 1 : 0);
     } else {
       const int S = gridDim.x;
       t = blockIdx.y;
@@ -153,13 +164,13 @@ struct SegIter {
       return a_hi > a_lo;
     }
     if (u >= u1) return false;
-    const long long tile = u / NA;
-    const int a0 = (int)(u - tile * NA);
-    const long long rem = u1 - u;
-    const int a1 = (rem < (long long)(NA - a0)) ? a0 + (int)rem : NA;
-    s.tile = (int)tile;
-    s.t = (int)(tile / m_tiles);
-    s.mt = (int)(tile - (long long)s.t * m_tiles);
+    const int tile = u / NA;
+    const int a0 = u - tile * NA;
+    const int rem = u1 - u;
+    const int a1 = (rem < NA - a0) ? a0 + rem : NA;
+    s.tile = tile;
+    s.t = tile / m_tiles;
+    s.mt = tile - s.t * m_tiles;
     s.a_lo = a0;
     s.a_hi = a1;
     u += (a1 - a0);
@@ -167,12 +178,11 @@ struct SegIter {
   }
 };
 
-// stream-K bookkeeping: CTA owning unit u, and a CTA's first unit
-__device__ __forceinline__ int sk_cta_of(long long u, long long U, int P) {
-  return (int)(((u + 1) * P - 1) / U);
-}
-__device__ __forceinline__ long long sk_start(int c, long long U, int P) {
-  return ((long long)c * U) / P;
+// stream-K bookkeeping (U = P q + r, KParams): a CTA's first unit, and the CTA owning unit u
+__device__ __forceinline__ int sk_start(int c, int q, int r) { return c * q + min(c, r); }
+__device__ __forceinline__ int sk_cta_of(int u, int q, int r) {
+  const int b = r * (q + 1);   // units owned by the r CTAs with q + 1 units
+  return u < b ? u / (q + 1) : r + (u - b) / q;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -191,12 +201,11 @@ struct DequantConsts {
 };
 
 __device__ __forceinline__ DequantConsts make_consts(uint32_t sbits, uint32_t z) {
+  // both halves replicated with PRMT (ALU pipe; the FMA pipe is the dequant's bottleneck)
   DequantConsts c;
-  const uint32_t lo = 0x6400u + z;          // 1024 + z   (ulp 1 in [1024, 2048))
-  const uint32_t hi = 0xD400u + 16u * z;    // -(64 + z)  (ulp 1/16 in [64, 128))
-  c.zlo = lo | (lo << 16);
-  c.zhi = hi | (hi << 16);
-  c.s2 = sbits | (sbits << 16);
+  c.zlo = __byte_perm(0x6400u + z, 0u, 0x1010);          // 1024 + z   (ulp 1 in [1024, 2048))
+  c.zhi = __byte_perm(0xD400u + (z << 4), 0u, 0x1010);   // -(64 + z)  (ulp 1/16 in [64, 128))
+  c.s2 = __byte_perm(sbits, 0u, 0x1010);
   return c;
 }
 
@@ -256,10 +265,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
   constexpr int APL = C::APL;
   constexpr int kAStages = C::ASTAGES;
   constexpr int kDCol = C::DCOL;
+  if (p.flags & kDebugExitTop) return;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  const uint32_t sbase = ptx::smem_u32(smem);
+  // 1 KiB-aligned base, computed in the 32-bit shared window (cheap to rematerialise)
+  const uint32_t sraw = ptx::smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sbase - sraw);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int K = p.K, G = p.G, M = p.M;
@@ -282,7 +293,10 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::HOLD_OFF);
   volatile int* sk_flag = reinterpret_cast<volatile int*>(smem + C::HOLD_OFF + 4);
 
-  if (threadIdx.x == 0) {
+  // Prologue.  The producer initialises the barriers and starts loading at once; the other
+  // warps wait on named barrier 2 (which orders the inits before them) while the MMA warp
+  // allocates TMEM, so the first loads are not held up by the allocation.
+  if (threadIdx.x == kProducerWarp * 32) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
       // 128 dequant-thread arrivals per A stage of the load stage (a thread reading the only A
@@ -299,12 +313,27 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
-  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), C::TMEM_COLS);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
+  uint32_t tmem = 0;
+  if (warp == kProducerWarp) {
+    if (lane == 0) ptx::prefetch_tmap(&tmap_x);
+    __syncwarp();
+    ptx::named_bar_arrive(2, kThreads);
+  } else {
+    if (warp == kMmaWarp) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), C::TMEM_COLS);
+    ptx::tc_fence_before();
+    ptx::named_bar_sync(2, kThreads);
+    ptx::tc_fence_after();
+    tmem = *tmem_holder;
+  }
+  if (p.flags & kDebugExitPrologue) {
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+    return;
+  }
   // debug tracing (TRACE instantiation only, tools/trace_gemm.py): clock64 stamps per stage
   unsigned long long* tr = nullptr;
   const unsigned lin16 = SK ? blockIdx.x : blockIdx.y * gridDim.x + blockIdx.x;
@@ -319,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
   // this grid's completion before touching anything this grid writes
   ptx::griddep_launch_dependents();
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------------------ producer
     // The whole warp runs the (warp-uniform) loop; one elected lane issues the copies, so the
     // addresses stay in uniform registers and no per-lane waterfall is generated.  Load
@@ -371,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; one elected lane issues the MMAs and the commits (a commit tracks
     // the async tcgen05 ops of the thread that issues it, so the same lane does both).
@@ -385,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
       const int db = SK ? (si & 1) : 0;
       // stream-K: the accumulator of segment si - 2 must have been read out
       if (SK && si >= 2) ptx::mbar_wait(bar_dempty + 8 * db, (uint32_t)(((si >> 1) + 1) & 1));
-      const uint32_t d_col = tmem + kDCol + (uint32_t)(db * BN);
+      const uint32_t d_col = tmem + kDCol + (uint32_t)(db * C::NACC * BN);
       int sub = 0;
       for (int a = sg.a_lo; a < sg.a_hi; ++a, ++ia) {
         // A stage written by the 4 warps of its parity group; they waited on `full`, which
@@ -396,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         const int kv = min(kKA, K - a * kKA);   // 128, or 64 at the end of K
         const bool last_of_load = (sub == APL - 1) || (a == sg.a_hi - 1);
         if (ptx::elect_one()) {
-          if (dbg_nocompute) {
+          if (dbg_nocompute || (p.flags & kDebugNoMma)) {
             ptx::mma_commit(bar_aempty + 8 * as);
             if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);
             if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
@@ -408,9 +437,9 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
 #pragma unroll
           for (int kk = 0; kk < kKA / 16; ++kk) {
             if (kk * 16 < kv)
-              ptx::mma_f16_ts(d_col, a_col + kk * 8,
+              ptx::mma_f16_ts(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
                               dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
-                              (first && kk == 0) ? 0u : 1u);
+                              (first && kk < C::NACC) ? 0u : 1u);
           }
           ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
           if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage used
@@ -443,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     // 32-k chunk otherwise.  Every thread arrives on the barriers itself.  After each segment
     // the same warps run its epilogue (their TMEM lanes, half of the columns each).
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int par = (warp - 2) >> 2;     // parity of the A stages this warp dequantizes
+    const int par = warp >> 2;           // parity of the A stages this warp dequantizes
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
     // 32-bit shared-window addresses: explicit ld.shared (a generic pointer through the
@@ -455,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     auto consts_at = [&](uint32_t mo) {
       return make_consts(ptx::lds_u16(mrow + mo), (ptx::lds_u8(zrow + mo) >> zsh) & 0xFu);
     };
-    const bool tw = TRACE && (warp == 2 && lane == 0);
+    const bool tw = TRACE && (warp == 0 && lane == 0);
     constexpr int kColsPerWarp = BN / 2;
     const int j0 = par * kColsPerWarp;   // this warp's half of the accumulator columns
     uint32_t a_regs[32];
@@ -466,90 +495,104 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
       int g_prev = -1;                   // group constants are per tile: reset per segment
       DequantConsts cst = make_consts(0, 0);
       const int k_seg_end = min(sg.a_hi * kKA, K);
-      for (int a = sg.a_lo; a < sg.a_hi; ++a, ++ia) {
-        if ((ia & 1) != par) continue;
-        const int ka = a * kKA;
-        const int rel = a - sg.a_lo;
-        const int lf = lbase + rel / APL;        // flat load stage of this A stage
-        const int sub = rel - (rel / APL) * APL;
-        const int slot = lf % STAGES;
-        ptx::mbar_wait(bar_full + 8 * slot, (uint32_t)((lf / STAGES) & 1));
-        if (tw) stamp(2, ia);
-        const int g0 = group_of(ka - sub * kKA);
-        const uint32_t wp = wrow + slot * C::W_BYTES + sub * 4 * kChunkBytes;
-        const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
-        const bool full_stage = (ka + kKA) <= k_seg_end;
-        uint4 w[4];
-        w[0] = ptx::lds128(wp);
-        w[1] = ptx::lds128(wp + kChunkBytes);
-        if (full_stage) {
+      // This warp's A stages in the segment: every other one, starting at the first whose
+      // flat index has its parity.  With APL in {1, 2} the A stage's position inside its load
+      // stage (sub) is the same for all of them, and the load stage advances by 2 / APL per
+      // step, so slot / phase / A-ring indices are kept incrementally (no divisions).
+      {
+        const int rel0 = (par - ia) & 1;
+        const int sub = rel0 % APL;
+        int lf = lbase + rel0 / APL;
+        int slot = lf % STAGES;
+        uint32_t fph = (uint32_t)((lf / STAGES) & 1);
+        int iw = ia + rel0;
+        int as = iw % kAStages;
+        uint32_t aph = (uint32_t)((iw / kAStages) & 1);
+        const uint32_t sub_off = (uint32_t)(sub * 4 * kChunkBytes);
+        for (int a = sg.a_lo + rel0; a < sg.a_hi; a += 2, iw += 2) {
+          const int ka = a * kKA;
+          ptx::mbar_wait(bar_full + 8 * slot, fph);
+          if (tw) stamp(2, iw);
+          const uint32_t wp = wrow + (uint32_t)(slot * C::W_BYTES) + sub_off;
+          const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
+          const int g0 = GBIG ? ((ka - sub * kKA) >> g_shift) : group_of(ka - sub * kKA);
+          // all four 16-B chunks: a short last stage (K % 128 == 64) reads two stale chunks of
+          // its own slot and ignores them
+          uint4 w[4];
+          w[0] = ptx::lds128(wp);
+          w[1] = ptx::lds128(wp + kChunkBytes);
           w[2] = ptx::lds128(wp + 2 * kChunkBytes);
           w[3] = ptx::lds128(wp + 3 * kChunkBytes);
-        } else {
-          w[2] = make_uint4(0, 0, 0, 0);
-          w[3] = w[2];
-        }
-        DequantConsts cst1;
-        if constexpr (GBIG) {
-          const int g = group_of(ka);
-          if (g != g_prev) {
-            cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
-            g_prev = g;
+          DequantConsts cst1;
+          if constexpr (GBIG) {
+            const int g = ka >> g_shift;
+            if (g != g_prev) {
+              cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
+              g_prev = g;
+            }
+          } else {
+            cst = consts_at(moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes);
+            cst1 = consts_at(moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes);
           }
-        } else {
-          cst = consts_at(moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes);
-          cst1 = consts_at(moff + (uint32_t)(group_of(ka + 32) - g0) * kMetaBytes);
-        }
-        // one arrival per thread per A stage; a load stage holding a single A stage (end of a
-        // segment) gets the other parity's share from the same thread
-        const int in_load = min(APL, sg.a_hi - (a - sub));
-        ptx::mbar_arrive_cnt(bar_empty + 8 * slot, (uint32_t)(APL - in_load + 1));
-        if (dbg_nocompute) {
-          const int as0 = ia % kAStages;
-          ptx::mbar_wait(bar_aempty + 8 * as0, (uint32_t)(((ia / kAStages) & 1) ^ 1));
-          ptx::mbar_arrive(bar_afull + 8 * as0);
-          continue;
-        }
-        const int as = ia % kAStages;
-        const uint32_t aph = (uint32_t)((ia / kAStages) & 1);
-        dequant_word(w[0].x, cst, a_regs + 0);
-        dequant_word(w[0].y, cst, a_regs + 4);
-        dequant_word(w[0].z, cst, a_regs + 8);
-        dequant_word(w[0].w, cst, a_regs + 12);
-        const DequantConsts& c1 = GBIG ? cst : cst1;
-        dequant_word(w[1].x, c1, a_regs + 16);
-        dequant_word(w[1].y, c1, a_regs + 20);
-        dequant_word(w[1].z, c1, a_regs + 24);
-        dequant_word(w[1].w, c1, a_regs + 28);
-        ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
-        if (tw) stamp(3, ia);
-        ptx::tc_fence_after();
-        const uint32_t acol = tmem + tlane + as * kAColsPerStage;
-        ptx::tmem_st_32x32b_x32(acol, a_regs);
-        if (full_stage) {
-          DequantConsts cst2, cst3;
-          if constexpr (!GBIG) {
-            cst2 = consts_at(moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes);
-            cst3 = consts_at(moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes);
+          // one arrival per thread per A stage; a load stage holding a single A stage (end of
+          // a segment) gets the other parity's share from the same thread
+          const uint32_t cnt = (APL == 2 && sub == 0 && a + 1 >= sg.a_hi) ? 2u : 1u;
+          ptx::mbar_arrive_cnt(bar_empty + 8 * slot, cnt);
+          if (dbg_nocompute) {
+            ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+            ptx::mbar_arrive(bar_afull + 8 * as);
+          } else {
+            dequant_word(w[0].x, cst, a_regs + 0);
+            dequant_word(w[0].y, cst, a_regs + 4);
+            dequant_word(w[0].z, cst, a_regs + 8);
+            dequant_word(w[0].w, cst, a_regs + 12);
+            const DequantConsts& c1 = GBIG ? cst : cst1;
+            dequant_word(w[1].x, c1, a_regs + 16);
+            dequant_word(w[1].y, c1, a_regs + 20);
+            dequant_word(w[1].z, c1, a_regs + 24);
+            dequant_word(w[1].w, c1, a_regs + 28);
+            ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
+            if (tw) stamp(3, iw);
+            ptx::tc_fence_after();
+            const uint32_t acol = tmem + tlane + (uint32_t)(as * kAColsPerStage);
+            ptx::tmem_st_32x32b_x32(acol, a_regs);
+            if ((ka + kKA) <= k_seg_end) {   // second half (all but a short last stage)
+              DequantConsts cst2, cst3;
+              if constexpr (!GBIG) {
+                cst2 = consts_at(moff + (uint32_t)(group_of(ka + 64) - g0) * kMetaBytes);
+                cst3 = consts_at(moff + (uint32_t)(group_of(ka + 96) - g0) * kMetaBytes);
+              }
+              const DequantConsts& c2 = GBIG ? cst : cst2;
+              const DequantConsts& c3 = GBIG ? cst : cst3;
+              uint32_t b_regs[32];
+              dequant_word(w[2].x, c2, b_regs + 0);
+              dequant_word(w[2].y, c2, b_regs + 4);
+              dequant_word(w[2].z, c2, b_regs + 8);
+              dequant_word(w[2].w, c2, b_regs + 12);
+              dequant_word(w[3].x, c3, b_regs + 16);
+              dequant_word(w[3].y, c3, b_regs + 20);
+              dequant_word(w[3].z, c3, b_regs + 24);
+              dequant_word(w[3].w, c3, b_regs + 28);
+              ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(bar_afull + 8 * as);
+            if (tw) stamp(4, iw);
           }
-          const DequantConsts& c2 = GBIG ? cst : cst2;
-          const DequantConsts& c3 = GBIG ? cst : cst3;
-          uint32_t b_regs[32];
-          dequant_word(w[2].x, c2, b_regs + 0);
-          dequant_word(w[2].y, c2, b_regs + 4);
-          dequant_word(w[2].z, c2, b_regs + 8);
-          dequant_word(w[2].w, c2, b_regs + 12);
-          dequant_word(w[3].x, c3, b_regs + 16);
-          dequant_word(w[3].y, c3, b_regs + 20);
-          dequant_word(w[3].z, c3, b_regs + 24);
-          dequant_word(w[3].w, c3, b_regs + 28);
-          ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+          slot += 2 / APL;
+          if (slot >= STAGES) {
+            slot -= STAGES;
+            fph ^= 1u;
+          }
+          as += 2;
+          if (as >= kAStages) {
+            as -= kAStages;
+            aph ^= 1u;
+          }
         }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(bar_afull + 8 * as);
-        if (tw) stamp(4, ia);
       }
+      ia += sg.a_hi - sg.a_lo;
       lbase += (sg.a_hi - sg.a_lo + APL - 1) / APL;
 
       // ---------------------------------------------------------------- segment epilogue
@@ -558,8 +601,23 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
       const int n = sg.t * kTileRows + r;
       ptx::mbar_wait(bar_dfull + 8 * db, (uint32_t)((si >> 1) & 1));
       ptx::tc_fence_after();
-      if (TRACE && tr != nullptr && warp == 2 && lane == 0) tr[1] = clock64();
-      const uint32_t dcol = tmem + tlane + kDCol + (uint32_t)(db * BN);
+      if (TRACE && tr != nullptr && warp == 0 && lane == 0) tr[1] = clock64();
+      const uint32_t dcol = tmem + tlane + kDCol + (uint32_t)(db * C::NACC * BN);
+      // 8 accumulator columns of this thread's row; with NACC = 2 the two partial sums are
+      // added here (fixed order: even K=16 steps + odd K=16 steps)
+      auto load_d = [&](int jc, uint32_t (&v)[8]) {
+        ptx::tmem_ld_32x32b_x8(dcol + jc, v);
+        if constexpr (C::NACC == 2) {
+          uint32_t v2[8];
+          ptx::tmem_ld_32x32b_x8(dcol + BN + jc, v2);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(v2[i]));
+        } else {
+          ptx::tmem_wait_ld();
+        }
+      };
       const bool whole = SK ? (sg.a_lo == 0 && sg.a_hi == p.NA) : (S == 1);
       const int jmax = min(j0 + kColsPerWarp, M - m0);   // valid tokens (columns)
       if (whole) {
@@ -567,8 +625,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
 #pragma unroll 1
         for (int jc = j0; jc < jmax; jc += 8) {
           uint32_t v[8];
-          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
-          ptx::tmem_wait_ld();
+          load_d(jc, v);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int m = m0 + jc + i;
@@ -587,8 +644,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
 #pragma unroll 1
         for (int jc = j0; jc < j0 + kColsPerWarp; jc += 8) {
           uint32_t v[8];
-          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
-          ptx::tmem_wait_ld();
+          load_d(jc, v);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             ptx::sts_u32(sbase + (uint32_t)(((jc + i) * kTileRows + r) * 4), v[i]);
@@ -600,8 +656,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
 #pragma unroll 1
         for (int jc = j0; jc < jmax; jc += 8) {
           uint32_t v[8];
-          ptx::tmem_ld_32x32b_x8(dcol + jc, v);
-          ptx::tmem_wait_ld();
+          load_d(jc, v);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             if (jc + i < jmax) __stcg(slot_ws + (jc + i) * kTileRows + r, __uint_as_float(v[i]));
@@ -609,23 +664,26 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         // the accumulator has been read: let the MMA reuse it before the cross-CTA fix-up
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar_dempty + 8 * db);
-        const long long u_first = (long long)sg.tile * p.NA;
-        const int c_first = sk_cta_of(u_first, p.U, p.P);
-        const int c_last = sk_cta_of(u_first + p.NA - 1, p.U, p.P);
-        __threadfence();
+        const int u_first = sg.tile * p.NA;
+        const int c_first = sk_cta_of(u_first, p.sk_q, p.sk_r);
+        const int c_last = sk_cta_of(u_first + p.NA - 1, p.sk_q, p.sk_r);
+        // publish: the named barrier orders every partial store of the CTA before thread 0's
+        // gpu-scope fence + arrival (fence cumulativity), so one thread fences, not 256
         ptx::named_bar_sync(1, kDqThreads);
-        if (threadIdx.x == 64) {
+        if (threadIdx.x == 0) {
+          __threadfence();
           const int prev = atomicAdd(p.sems + sg.tile, 1);
-          *sk_flag = (prev == c_last - c_first) ? 1 : 0;
+          const int last = (prev == c_last - c_first) ? 1 : 0;
+          if (last) __threadfence();   // acquire: the other CTAs' partials, before the barrier
+          *sk_flag = last;
         }
         ptx::named_bar_sync(1, kDqThreads);
         if (*sk_flag) {
           // last arriver: sum the partials of CTAs c_first..c_last in that order (deterministic),
           // the tile spread over the 256 dequant threads as float4 columns-of-rows, with up to
-          // 4 partial loads in flight before the in-order adds
-          __threadfence();
+          // 4 partial loads (ld.global.cg: L2, never a stale L1 line) in flight before the adds
           const int jvalid = min(BN, M - m0);
-          const int tid = (int)threadIdx.x - 64;
+          const int tid = (int)threadIdx.x;
           for (int e4 = tid; e4 < jvalid * (kTileRows / 4); e4 += kDqThreads) {
             const int j = e4 / (kTileRows / 4);
             const int r4 = (e4 % (kTileRows / 4)) * 4;
@@ -636,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
               for (int u = 0; u < 4; ++u) {
                 const int c = c0 + u;
                 if (c <= c_last) {
-                  const int sl = (sk_start(c, p.U, p.P) >= u_first) ? 0 : 1;
+                  const int sl = (sk_start(c, p.sk_q, p.sk_r) >= u_first) ? 0 : 1;
                   v[u] = __ldcg(reinterpret_cast<const float4*>(
                       p.ws + ((size_t)c * 2 + sl) * (BN * kTileRows) + j * kTileRows + r4));
                 }
@@ -663,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
               *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
             }
           }
-          if (threadIdx.x == 64) p.sems[sg.tile] = 0;   // self-reset for the next launch
+          if (threadIdx.x == 0) p.sems[sg.tile] = 0;   // self-reset for the next launch
         }
       }
       if (SK && whole) {
@@ -744,7 +802,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tr[4] = smid;
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, C::TMEM_COLS);
   }
@@ -925,7 +983,8 @@ cudaError_t configure_kernel(int bn, bool sk) {
   // shared memory: two 80-110 KiB CTAs per SM
   for (int v = 0; v < 4 && e == cudaSuccess; ++v) {
     void* k = (v & 2) ? trace_kernel_for(bn, sk, v & 1) : kernel_for(bn, sk, v & 1);
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(bn, sk));
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             std::max(smem_for(bn, sk), 120 * 1024));   // 120 KiB: kDebugOneCta
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
                                (int)cudaSharedmemCarveoutMaxShared);
@@ -1066,14 +1125,14 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
   const int tiles = (N / quick::kTileRows) * ((M + tn - 1) / tn);
-  if (allow_sk && force_split == 0 && sk_capable(tn)) {
+  if (allow_sk && force_split == 0 && sk_capable(tn) && (long long)tiles * NA < (1LL << 30)) {
     const long long U = (long long)tiles * NA;
     const long long resident = (long long)max_resident(tn, true, 1);
     long long P = std::min(resident, std::max(1LL, U / 4));
     // accuracy: a CTA's segment of one tile spans at most kMaxAccumK of K
     const long long p_min = (U * quick::kKA + kMaxAccumK - 1) / kMaxAccumK;
     if (P < p_min) P = std::min(resident, p_min);
-    if (U / P <= kMaxAccumK / quick::kKA) return Plan{tn, 1, (int)P, true, (int)P};
+    if ((U + P - 1) / P <= kMaxAccumK / quick::kKA) return Plan{tn, 1, (int)P, true, (int)P};
   }
   int S = 1;
   if (force_split > 0) {
@@ -1105,6 +1164,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
     cfg.gridDim = dim3((unsigned)S, (unsigned)kp.n_tiles, (unsigned)kp.m_tiles);
   cfg.blockDim = dim3(quick::kThreads, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  if (kp.flags & quick::kDebugOneCta) cfg.dynamicSmemBytes = std::max<size_t>(C::SMEM_BYTES, 120 * 1024);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -1123,7 +1183,9 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   cfg.attrs = attr;
   cfg.numAttrs = na;
   kp.trace = g_trace;
-  const bool gbig = (kp.G % quick::kKA) == 0;
+  // group-size specialisation: a power of two >= 128 (the group index is a shift and an A
+  // stage never straddles groups); any other G takes the per-32-k general path
+  const bool gbig = kp.G >= quick::kKA && (kp.G & (kp.G - 1)) == 0;
   if (g_trace != nullptr)
     e = gbig ? cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true, true>, tmap, kp)
              : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, true>, tmap, kp);
@@ -1180,7 +1242,9 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (M == 0) return QUICK_OK;
   if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
-  const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute;
+  const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
+                    quick::kDebugExitTop | quick::kDebugExitPrologue |
+                    quick::kDebugNoMma | quick::kDebugOneCta;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1189,6 +1253,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
 
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
   Plan plan = choose_plan(M, N, K, G, tile_n, split_k, (flags & QUICK_FLAG_NO_STREAMK) == 0);
+  if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
   quick::KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.n_tiles = N / quick::kTileRows;
@@ -1235,8 +1300,10 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   kp.ldy = ldy;
   kp.flags = flags;
   kp.NA = NA;
-  kp.U = (long long)kp.n_tiles * kp.m_tiles * NA;
+  kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;
+  kp.sk_q = kp.U / max(kp.P, 1);
+  kp.sk_r = kp.U - kp.sk_q * max(kp.P, 1);
   if (plan.sk) {
     switch (tn) {
       case 16: return launch_bn<16, true>(tmap, kp, 1, plan.P, strm);

@@ -19,6 +19,7 @@ ap.add_argument("--G", type=int, default=128)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--tile_n", type=int, default=0)
 ap.add_argument("--split_k", type=int, default=0)
+ap.add_argument("--flags", type=lambda v: int(v, 0), default=0)
 a = ap.parse_args()
 p = synth.make_problem(0, a.M, a.N, a.K, a.G)
 blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, a.G)).cuda()
@@ -26,6 +27,11 @@ copies = [blob] + [blob.clone() for _ in range(a.reps - 1)]
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((a.M, a.N), device="cuda", dtype=torch.float16)
 for r in range(a.reps):
-    quick.quick_w4a16_gemm(x, copies[r], a.N, a.K, a.G, out=y, tile_n=a.tile_n, split_k=a.split_k)
+    if a.flags:
+        quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[r].data_ptr(), a.M, a.N, a.K, a.G, y.data_ptr(),
+                                   torch.cuda.current_stream().cuda_stream, flags=a.flags, tile_n=a.tile_n,
+                                   split_k=a.split_k)
+    else:
+        quick.quick_w4a16_gemm(x, copies[r], a.N, a.K, a.G, out=y, tile_n=a.tile_n, split_k=a.split_k)
 torch.cuda.synchronize()
 print("plan", quick.quick_gemm_plan(a.M, a.N, a.K, a.G))
