@@ -117,8 +117,8 @@ struct KParams {
   // (32-bit, no division on the device); partial tiles go through ws and are summed by the
   // last arriver
   int U, P, sk_q, sk_r;
-  float* ws;              // [P][2][BN][128] fp32 partial tiles (slot 0: first segment, 1: last)
-  int* sems;              // [tiles] arrival counters, zero between launches (self-resetting)
+  float* ws;              // [P][BN][128] fp32 partial tile of each CTA's (only) non-reducer segment
+  int* sems;              // [tiles] arrival counters, zero between launches (reset by the reducer)
   unsigned long long* trace;
 };
 
@@ -291,7 +291,6 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
   const uint32_t bar_dfull = bar_aempty + 8 * kAStages;   // [2]
   const uint32_t bar_dempty = bar_dfull + 16;             // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::HOLD_OFF);
-  volatile int* sk_flag = reinterpret_cast<volatile int*>(smem + C::HOLD_OFF + 4);
 
   // Prologue.  The producer initialises the barriers and starts loading at once; the other
   // warps wait on named barrier 2 (which orders the inits before them) while the MMA warp
@@ -650,78 +649,68 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
             ptx::sts_u32(sbase + (uint32_t)(((jc + i) * kTileRows + r) * 4), v[i]);
         }
       } else {
-        // stream-K partial tile: fp32 into this CTA's workspace slot (0: first segment, 1: the
-        // last), then the last CTA to arrive on the tile sums every partial in CTA order
-        float* slot_ws = p.ws + ((size_t)blockIdx.x * 2 + (si == 0 ? 0 : 1)) * (BN * kTileRows);
-#pragma unroll 1
-        for (int jc = j0; jc < jmax; jc += 8) {
-          uint32_t v[8];
-          load_d(jc, v);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (jc + i < jmax) __stcg(slot_ws + (jc + i) * kTileRows + r, __uint_as_float(v[i]));
-        }
-        // the accumulator has been read: let the MMA reuse it before the cross-CTA fix-up
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(bar_dempty + 8 * db);
+        // stream-K partial tile.  The tile's units are owned by CTAs c_first..c_last in k
+        // order; c_first reaches them at the END of its range (its last segment), the others
+        // at the start of theirs, so c_first is the fixed reducer: the others store an fp32
+        // partial [BN][128] into their workspace slot and post a release increment without
+        // waiting; c_first waits (rarely for long) for all of them, adds their partials in CTA
+        // order to its own accumulator (straight from TMEM) and writes Y.  Deterministic.
         const int u_first = sg.tile * p.NA;
         const int c_first = sk_cta_of(u_first, p.sk_q, p.sk_r);
         const int c_last = sk_cta_of(u_first + p.NA - 1, p.sk_q, p.sk_r);
-        // publish: the named barrier orders every partial store of the CTA before thread 0's
-        // gpu-scope fence + arrival (fence cumulativity), so one thread fences, not 256
-        ptx::named_bar_sync(1, kDqThreads);
-        if (threadIdx.x == 0) {
-          __threadfence();
-          const int prev = atomicAdd(p.sems + sg.tile, 1);
-          const int last = (prev == c_last - c_first) ? 1 : 0;
-          if (last) __threadfence();   // acquire: the other CTAs' partials, before the barrier
-          *sk_flag = last;
-        }
-        ptx::named_bar_sync(1, kDqThreads);
-        if (*sk_flag) {
-          // last arriver: sum the partials of CTAs c_first..c_last in that order (deterministic),
-          // the tile spread over the 256 dequant threads as float4 columns-of-rows, with up to
-          // 4 partial loads (ld.global.cg: L2, never a stale L1 line) in flight before the adds
-          const int jvalid = min(BN, M - m0);
-          const int tid = (int)threadIdx.x;
-          for (int e4 = tid; e4 < jvalid * (kTileRows / 4); e4 += kDqThreads) {
-            const int j = e4 / (kTileRows / 4);
-            const int r4 = (e4 % (kTileRows / 4)) * 4;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int c0 = c_first; c0 <= c_last; c0 += 4) {
-              float4 v[4];
+        int* sem = p.sems + sg.tile;
+        if ((int)blockIdx.x != c_first) {
+          float* slot_ws = p.ws + (size_t)blockIdx.x * (BN * kTileRows);
+#pragma unroll 1
+          for (int jc = j0; jc < jmax; jc += 8) {
+            uint32_t v[8];
+            load_d(jc, v);
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int c = c0 + u;
-                if (c <= c_last) {
-                  const int sl = (sk_start(c, p.sk_q, p.sk_r) >= u_first) ? 0 : 1;
-                  v[u] = __ldcg(reinterpret_cast<const float4*>(
-                      p.ws + ((size_t)c * 2 + sl) * (BN * kTileRows) + j * kTileRows + r4));
-                }
-              }
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                if (c0 + u <= c_last) {
-                  acc.x += v[u].x;
-                  acc.y += v[u].y;
-                  acc.z += v[u].z;
-                  acc.w += v[u].w;
-                }
-              }
+            for (int i = 0; i < 8; ++i)
+              if (jc + i < jmax) __stcg(slot_ws + (jc + i) * kTileRows + r, __uint_as_float(v[i]));
+          }
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(bar_dempty + 8 * db);   // the accumulator has been read
+          // the named barrier orders every partial store of the CTA before thread 0's gpu-scope
+          // release (cumulativity); nobody waits for the increment itself
+          ptx::named_bar_sync(1, kDqThreads);
+          if (threadIdx.x == 0) ptx::red_release_gpu_add(sem, 1);
+        } else {
+          if (threadIdx.x == 0) {
+            const int want = c_last - c_first;
+            while (ptx::ld_acquire_gpu(sem) < want) {
             }
-            const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)sg.t * kTileRows + r4;
-            if (out_fp32) {
-              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
-            } else {
-              __half2 lo = __floats2half2_rn(acc.x, acc.y);
-              __half2 hi = __floats2half2_rn(acc.z, acc.w);
-              uint2 pk;
-              pk.x = *reinterpret_cast<uint32_t*>(&lo);
-              pk.y = *reinterpret_cast<uint32_t*>(&hi);
-              *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
+            *sem = 0;   // self-reset for the next launch (no one else touches it until then)
+          }
+          ptx::named_bar_sync(1, kDqThreads);   // acquire -> every reader thread
+#pragma unroll 1
+          for (int jc = j0; jc < jmax; jc += 8) {
+            uint32_t v[8];
+            load_d(jc, v);
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = __uint_as_float(v[i]);
+            for (int c = c_first + 1; c <= c_last; ++c) {
+              const float* pw = p.ws + (size_t)c * (BN * kTileRows) + (size_t)jc * kTileRows + r;
+              float pv[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pv[i] = (jc + i < jmax) ? __ldcg(pw + i * kTileRows) : 0.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] += pv[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int m = m0 + jc + i;
+              if (jc + i < jmax) {
+                if (out_fp32)
+                  reinterpret_cast<float*>(p.Y)[(size_t)m * p.ldy + n] = acc[i];
+                else
+                  reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(acc[i]);
+              }
             }
           }
-          if (threadIdx.x == 0) p.sems[sg.tile] = 0;   // self-reset for the next launch
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(bar_dempty + 8 * db);
         }
       }
       if (SK && whole) {
@@ -1261,7 +1250,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (plan.sk) {
     float* ws = nullptr;
     int* sems = nullptr;
-    const size_t ws_bytes = (size_t)plan.P * 2 * plan.tile_n * quick::kTileRows * sizeof(float);
+    const size_t ws_bytes = (size_t)plan.P * plan.tile_n * quick::kTileRows * sizeof(float);
     if (get_workspace(strm, ws_bytes, (size_t)kp.n_tiles * kp.m_tiles, &ws, &sems)) {
       kp.ws = ws;
       kp.sems = sems;

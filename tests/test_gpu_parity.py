@@ -143,7 +143,7 @@ def test_llama7b_attention_sweep(M):
                                      (9, 4096, 4096, 128), (16, 28672, 1024, 128)])
 def test_stream_k_segments(M, N, K, G):
     """Stream-K (auto plan, tiles <= 64): CTAs own unit ranges that cross tile boundaries;
-    partial tiles are summed by the last CTA in fixed order -- vs the oracle, vs the cluster
+    partial tiles are summed by the tile's first CTA in fixed order -- vs the oracle, vs the cluster
     split-K plan, and run-to-run bit-identical.  Shapes include odd A-stage counts and a
     64-k ragged tail (K % 128 == 64)."""
     p = synth.make_problem(M * 7 + K, M=M, N=N, K=K, G=G)
