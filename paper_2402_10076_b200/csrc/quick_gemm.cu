@@ -77,7 +77,7 @@ struct Cfg {
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
-  static constexpr int STAGES = BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 64 ? 4 : BN <= 128 ? 4 : 2;
+  static constexpr int STAGES = BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 64 ? 4 : BN <= 128 ? 4 : 3;
   static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
@@ -433,12 +433,21 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
           // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
           const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES + sub * 2 * C::X_SUB) >> 4);
           const bool first = (a == sg.a_lo);
+          if (kv == kKA && !first) {
+            // steady state: 8 unpredicated, always-accumulating MMAs (lean issue: the A-ring
+            // slot is held until these complete, so issue latency throttles the dequantizers)
 #pragma unroll
-          for (int kk = 0; kk < kKA / 16; ++kk) {
-            if (kk * 16 < kv)
-              ptx::mma_f16_ts(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
-                              dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
-                              (first && kk < C::NACC) ? 0u : 1u);
+            for (int kk = 0; kk < kKA / 16; ++kk)
+              ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
+                                  dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < kKA / 16; ++kk) {
+              if (kk * 16 < kv)
+                ptx::mma_f16_ts(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
+                                dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
+                                (first && kk < C::NACC) ? 0u : 1u);
+            }
           }
           ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
           if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage used
@@ -1121,7 +1130,12 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
     // accuracy: a CTA's segment of one tile spans at most kMaxAccumK of K
     const long long p_min = (U * quick::kKA + kMaxAccumK - 1) / kMaxAccumK;
     if (P < p_min) P = std::min(resident, p_min);
-    if ((U + P - 1) / P <= kMaxAccumK / quick::kKA) return Plan{tn, 1, (int)P, true, (int)P};
+    // stream-K pays when a CTA's range covers at least half a tile (each tile then has <= ~3
+    // contributors and the fix-up is short); when K is cut finer, the DSMEM cluster split-K
+    // reduce is cheaper than the workspace fix-up (measured on B200: 4096^2 and both 13B
+    // shapes favour the cluster, 28672x8192 stream-K)
+    if (2 * (U / P) >= NA && (U + P - 1) / P <= kMaxAccumK / quick::kKA)
+      return Plan{tn, 1, (int)P, true, (int)P};
   }
   int S = 1;
   if (force_split > 0) {

@@ -25,6 +25,8 @@ L = 32
 
 
 def timeit(fn_launch, reps=5):
+    fn_launch(0)   # eager first: the stream-K workspace is allocated outside capture
+    torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         for i in range(L):
