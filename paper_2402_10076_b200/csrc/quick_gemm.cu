@@ -39,10 +39,9 @@
 
 namespace quick {
 
-constexpr int kThreads = 320;     // 10 warps: 8 dequantizers (2 per TMEM lane quarter), producer, MMA
-constexpr int kProducerWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kDqThreads = 256;   // the 8 dequantizer warps (named barrier 1 in stream-K epilogues)
+// CTA shape per config (Cfg::NPAR dequant groups of 4 warps, one per TMEM lane quarter, then
+// the producer warp and the MMA warp on the top warp ids)
+constexpr int kMaxThreads = 18 * 32;
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
 constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
@@ -56,6 +55,7 @@ constexpr int kDebugExitTop = 1 << 29;     // debug: return at kernel entry (lau
 constexpr int kDebugExitPrologue = 1 << 28;  // debug: return after the prologue (setup probe)
 constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (commits only)
 constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
+constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -68,16 +68,29 @@ constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per S
 //          epilogue, because a single accumulator chain makes N=16 MMAs latency-bound)
 template <int BN, bool SK>
 struct Cfg {
+  // NPAR dequant groups of 4 warps.  NPAR = 4 (one CTA per SM, 16 dequant warps, the whole TMEM
+  // for a 6-7 slot A ring) was measured 1.9x slower per SM than two 2-group CTAs per SM on the
+  // 70B shapes at M <= 64 (one MMA warp per SM cannot keep up), so every tile uses 2 groups; the
+  // code is written for any power-of-two NPAR.
+  static constexpr int NPAR = 2;
+  static constexpr int THREADS = 32 * (4 * NPAR + 2);
+  static constexpr int PRODUCER_WARP = 4 * NPAR;
+  static constexpr int MMA_WARP = 4 * NPAR + 1;
+  static constexpr int DQ_THREADS = 128 * NPAR;
   static constexpr int NDBUF = SK ? 2 : 1;
+  static constexpr int TMEM_BUDGET = NPAR == 4 ? 512 : 256;
+  static constexpr int ASTAGES_FIT = (TMEM_BUDGET - NDBUF * (BN <= 32 ? 2 : 1) * BN) / kAColsPerStage;
   static constexpr int ASTAGES =
-      BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2);
+      NPAR == 4 ? (ASTAGES_FIT > 7 ? 7 : ASTAGES_FIT)
+                : (BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2));
   static constexpr int DCOL = ASTAGES * kAColsPerStage;
-  static constexpr int NACC = (BN <= 32 && DCOL + NDBUF * 2 * BN <= 256) ? 2 : 1;
+  static constexpr int NACC = (BN <= 32 && DCOL + NDBUF * 2 * BN <= TMEM_BUDGET) ? 2 : 1;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
-  static constexpr int STAGES = BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 64 ? 4 : BN <= 128 ? 4 : 3;
+  static constexpr int STAGES = NPAR == 4 ? (BN <= 16 ? 8 : BN <= 32 ? 6 : 8)
+                                          : (BN <= 128 ? 4 : 3);
   static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
@@ -90,7 +103,7 @@ struct Cfg {
   static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 4;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;   // TMEM base, then stream-K flag
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = (DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (NPAR == 2 && DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512;
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
   static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
@@ -99,6 +112,7 @@ struct Cfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
   static_assert(KL % kKA == 0 && APL <= 2, "load stage = one or two A stages");
   static_assert(!SK || BN <= 64, "stream-K is used for the small-M tiles");
+  static_assert(ASTAGES >= NPAR && STAGES * APL >= NPAR, "ring indices advance by NPAR per group step");
   static_assert(DCOL + NDBUF * NACC * BN <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // split-K partial tile [BN][128] fp32 reuses the pipeline buffers once the mainloop is done
@@ -257,10 +271,15 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
 }
 
 template <int BN, bool SK, bool GBIG, bool TRACE>
-__global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
+__global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const __grid_constant__ KParams p) {
   using C = Cfg<BN, SK>;
+  constexpr int kThreads = C::THREADS;
+  constexpr int kProducerWarp = C::PRODUCER_WARP;
+  constexpr int kMmaWarp = C::MMA_WARP;
+  constexpr int kDqThreads = C::DQ_THREADS;
+  constexpr int NPAR = C::NPAR;
   constexpr int STAGES = C::STAGES;
   constexpr int APL = C::APL;
   constexpr int kAStages = C::ASTAGES;
@@ -280,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
   const bool out_fp32 = (p.flags & QUICK_FLAG_OUT_F32) != 0;
   const bool pdl = (p.flags & QUICK_FLAG_PDL) != 0;
   const bool dbg_nocompute = (p.flags & kDebugNoCompute) != 0;   // load path only (debug)
+  const bool dbg_nosttm = (p.flags & kDebugNoSttm) != 0;
   const int g_shift = p.g_shift;
   // group index of k: shift when G is a power of two, division otherwise
   auto group_of = [&](int k) { return g_shift >= 0 ? (k >> g_shift) : (k / G); };
@@ -424,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         const int kv = min(kKA, K - a * kKA);   // 128, or 64 at the end of K
         const bool last_of_load = (sub == APL - 1) || (a == sg.a_hi - 1);
         if (ptx::elect_one()) {
-          if (dbg_nocompute || (p.flags & kDebugNoMma)) {
+          if (dbg_nocompute || (p.flags & (kDebugNoMma | kDebugNoSttm))) {
             ptx::mma_commit(bar_aempty + 8 * as);
             if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);
             if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
@@ -480,21 +500,40 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
     // 32-k chunk otherwise.  Every thread arrives on the barriers itself.  After each segment
     // the same warps run its epilogue (their TMEM lanes, half of the columns each).
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int par = warp >> 2;           // parity of the A stages this warp dequantizes
+    const int par = warp >> 2;           // group: A stages a with (a - first) % NPAR == par
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
     // 32-bit shared-window addresses: explicit ld.shared (a generic pointer through the
     // 1 KiB alignment cast compiles to slower generic LD.E)
-    const uint32_t wrow = sbase + C::W_OFF + r * 16;
-    const uint32_t mrow = sbase + C::M_OFF + r * 2;           // scale of row r in a meta block
-    const uint32_t zrow = sbase + C::M_OFF + 256 + (r >> 1);  // zero byte of row r
-    const uint32_t zsh = (uint32_t)(r & 1) * 4u;
+    // (the base is made opaque so the compiler keeps it in a register instead of
+    // re-deriving the aligned shared-window address in every iteration)
+    uint32_t sb = sbase;
+    asm volatile("" : "+r"(sb));
+    const uint32_t wrow = sb + C::W_OFF + r * 16;
+    const uint32_t mrow = sb + C::M_OFF + r * 2;           // scale of row r in a meta block
+    const uint32_t zrow = sb + C::M_OFF + 256 + (r >> 1);  // zero byte of row r
+    const uint32_t zsh = (uint32_t)(r & 1) * 4u;           // nibble of row r in its byte
+    const uint32_t zsh_hi = 4u - zsh;
+    int gsh = g_shift;                                     // kept in a register (no LDC per stage)
+    asm volatile("" : "+r"(gsh));
+    // group constants straight from the meta bytes (8 instructions): the zero byte is
+    // replicated into both fp16 halves with one PRMT, then shifted/masked into 1024 + z and
+    // -(64 + z) (bit-identical to make_consts)
     auto consts_at = [&](uint32_t mo) {
-      return make_consts(ptx::lds_u16(mrow + mo), (ptx::lds_u8(zrow + mo) >> zsh) & 0xFu);
+      const uint32_t zb = ptx::lds_u8(zrow + mo);
+      const uint32_t sbits = ptx::lds_u16(mrow + mo);
+      const uint32_t zr = __byte_perm(zb, 0u, 0x4040);   // [zb, 0, zb, 0]
+      DequantConsts c;
+      c.zlo = ptx::lop3<0xEA>(zr >> zsh, 0x000F000Fu, 0x64006400u);
+      c.zhi = ptx::lop3<0xEA>(zr << zsh_hi, 0x00F000F0u, 0xD400D400u);
+      c.s2 = __byte_perm(sbits, 0u, 0x1010);
+      return c;
     };
     const bool tw = TRACE && (warp == 0 && lane == 0);
-    constexpr int kColsPerWarp = BN / 2;
-    const int j0 = par * kColsPerWarp;   // this warp's half of the accumulator columns
+    // epilogue: the accumulator columns are split over the groups in chunks of >= 8
+    constexpr int kColsPerWarp = BN / NPAR >= 8 ? BN / NPAR : 8;
+    const int j0 = par * kColsPerWarp;   // this warp's share of the accumulator columns
+    const int jend = min(j0 + kColsPerWarp, BN);
     uint32_t a_regs[32];
     SegIter it(p, SK);
     Seg sg;
@@ -503,12 +542,13 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
       int g_prev = -1;                   // group constants are per tile: reset per segment
       DequantConsts cst = make_consts(0, 0);
       const int k_seg_end = min(sg.a_hi * kKA, K);
-      // This warp's A stages in the segment: every other one, starting at the first whose
-      // flat index has its parity.  With APL in {1, 2} the A stage's position inside its load
-      // stage (sub) is the same for all of them, and the load stage advances by 2 / APL per
-      // step, so slot / phase / A-ring indices are kept incrementally (no divisions).
+      // This warp's A stages in the segment: every NPAR-th one, starting at the first whose
+      // flat index is congruent to its group.  With APL in {1, 2} (dividing NPAR) the A stage's
+      // position inside its load stage (sub) is the same for all of them, and the load stage
+      // advances by NPAR / APL per step, so slot / phase / A-ring indices are kept
+      // incrementally (no divisions).
       {
-        const int rel0 = (par - ia) & 1;
+        const int rel0 = (par - ia) & (NPAR - 1);
         const int sub = rel0 % APL;
         int lf = lbase + rel0 / APL;
         int slot = lf % STAGES;
@@ -517,13 +557,13 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         int as = iw % kAStages;
         uint32_t aph = (uint32_t)((iw / kAStages) & 1);
         const uint32_t sub_off = (uint32_t)(sub * 4 * kChunkBytes);
-        for (int a = sg.a_lo + rel0; a < sg.a_hi; a += 2, iw += 2) {
+        for (int a = sg.a_lo + rel0; a < sg.a_hi; a += NPAR, iw += NPAR) {
           const int ka = a * kKA;
           ptx::mbar_wait(bar_full + 8 * slot, fph);
           if (tw) stamp(2, iw);
           const uint32_t wp = wrow + (uint32_t)(slot * C::W_BYTES) + sub_off;
           const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
-          const int g0 = GBIG ? ((ka - sub * kKA) >> g_shift) : group_of(ka - sub * kKA);
+          const int g0 = GBIG ? ((ka - sub * kKA) >> gsh) : group_of(ka - sub * kKA);
           // all four 16-B chunks: a short last stage (K % 128 == 64) reads two stale chunks of
           // its own slot and ignores them
           uint4 w[4];
@@ -533,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
           w[3] = ptx::lds128(wp + 3 * kChunkBytes);
           DequantConsts cst1;
           if constexpr (GBIG) {
-            const int g = ka >> g_shift;
+            const int g = ka >> gsh;
             if (g != g_prev) {
               cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
               g_prev = g;
@@ -563,6 +603,12 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
             if (tw) stamp(3, iw);
             ptx::tc_fence_after();
             const uint32_t acol = tmem + tlane + (uint32_t)(as * kAColsPerStage);
+            if (dbg_nosttm) {   // keep the dequant live without storing it
+              uint32_t x = 0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) x ^= a_regs[i];
+              if (x == 0x12345679u) ptx::tmem_st_32x32b_x32(acol, a_regs);
+            } else {
             ptx::tmem_st_32x32b_x32(acol, a_regs);
             if ((ka + kKA) <= k_seg_end) {   // second half (all but a short last stage)
               DequantConsts cst2, cst3;
@@ -581,19 +627,27 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
               dequant_word(w[3].y, c3, b_regs + 20);
               dequant_word(w[3].z, c3, b_regs + 24);
               dequant_word(w[3].w, c3, b_regs + 28);
-              ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+              if (dbg_nosttm) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) x ^= b_regs[i];
+                if (x == 0x12345679u) ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+              } else {
+                ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+              }
+            }
             }
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_afull + 8 * as);
             if (tw) stamp(4, iw);
           }
-          slot += 2 / APL;
+          slot += NPAR / APL;
           if (slot >= STAGES) {
             slot -= STAGES;
             fph ^= 1u;
           }
-          as += 2;
+          as += NPAR;
           if (as >= kAStages) {
             as -= kAStages;
             aph ^= 1u;
@@ -627,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         }
       };
       const bool whole = SK ? (sg.a_lo == 0 && sg.a_hi == p.NA) : (S == 1);
-      const int jmax = min(j0 + kColsPerWarp, M - m0);   // valid tokens (columns)
+      const int jmax = min(jend, M - m0);   // valid tokens (columns)
       if (whole) {
         // the full K range of this tile is in our accumulator: straight to Y
 #pragma unroll 1
@@ -650,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, Cfg<BN, SK>::MAX_CTAS_PER_SM)
         // cluster split-K: fp32 partial tile [BN][128] into our shared memory (pipeline buffers
         // are free: every stage has been consumed); reduced through DSMEM below
 #pragma unroll 1
-        for (int jc = j0; jc < j0 + kColsPerWarp; jc += 8) {
+        for (int jc = j0; jc < jend; jc += 8) {
           uint32_t v[8];
           load_d(jc, v);
 #pragma unroll
@@ -967,6 +1021,7 @@ void* trace_kernel_for(int bn, bool sk, bool gbig = true) { return kernel_for_t<
 QUICK_CFG_FIELD(tmem_cols_for, TMEM_COLS)
 QUICK_CFG_FIELD(kl_for, KL)
 QUICK_CFG_FIELD(smem_for, SMEM_BYTES)
+QUICK_CFG_FIELD(threads_for, THREADS)
 #undef QUICK_CFG_FIELD
 
 // one-time per (device, tile, mode): opt into the dynamic shared memory the config needs
@@ -1012,13 +1067,13 @@ int max_resident(int bn, bool sk, int S) {
       if (cudaFuncGetAttributes(&fa, kernel_for(bn, sk)) == cudaSuccess) regs = fa.numRegs;
       const int by_tmem = 512 / tmem_cols_for(bn, sk);
       const int by_smem = (228 * 1024) / (smem_for(bn, sk) + 1024);
-      const int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * (quick::kThreads / 32));
+      const int by_regs = 65536 / (((regs * 32 + 255) / 256) * 256 * (threads_for(bn, sk) / 32));
       n = std::max(1, std::min(by_tmem, std::min(by_smem, by_regs))) * sm_count();
     } else {
       cudaLaunchConfig_t cfg;
       std::memset(&cfg, 0, sizeof(cfg));
       cfg.gridDim = dim3((unsigned)S, 1, 1);
-      cfg.blockDim = dim3(quick::kThreads, 1, 1);
+      cfg.blockDim = dim3((unsigned)threads_for(bn, sk), 1, 1);
       cfg.dynamicSmemBytes = smem_for(bn, sk);
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeClusterDimension;
@@ -1134,7 +1189,8 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
     // contributors and the fix-up is short); when K is cut finer, the DSMEM cluster split-K
     // reduce is cheaper than the workspace fix-up (measured on B200: 4096^2 and both 13B
     // shapes favour the cluster, 28672x8192 stream-K)
-    if (2 * (U / P) >= NA && (U + P - 1) / P <= kMaxAccumK / quick::kKA)
+    // (a segment never spans more than one tile, so the accuracy cap only binds when NA > cap)
+    if (2 * (U / P) >= NA && (NA <= kMaxAccumK / quick::kKA || (U + P - 1) / P <= kMaxAccumK / quick::kKA))
       return Plan{tn, 1, (int)P, true, (int)P};
   }
   int S = 1;
@@ -1165,7 +1221,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
     cfg.gridDim = dim3((unsigned)P, 1, 1);
   else
     cfg.gridDim = dim3((unsigned)S, (unsigned)kp.n_tiles, (unsigned)kp.m_tiles);
-  cfg.blockDim = dim3(quick::kThreads, 1, 1);
+  cfg.blockDim = dim3((unsigned)C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   if (kp.flags & quick::kDebugOneCta) cfg.dynamicSmemBytes = std::max<size_t>(C::SMEM_BYTES, 120 * 1024);
   cfg.stream = stream;
@@ -1247,7 +1303,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
-                    quick::kDebugNoMma | quick::kDebugOneCta;
+                    quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;

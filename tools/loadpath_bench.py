@@ -34,7 +34,7 @@ def timeit(launch):
     return best
 
 
-SHAPES = [(16, 28672, 8192), (16, 4096, 4096), (16, 8192, 28672), (16, 13824, 5120)]
+SHAPES = [(16, 28672, 8192), (16, 4096, 4096), (16, 13824, 5120)]
 for (M, N, K) in SHAPES:
     p = synth.make_problem(0, M, N, K, 128)
     blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, 128)).cuda()
@@ -47,7 +47,9 @@ for (M, N, K) in SHAPES:
     quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y.data_ptr(), stream.cuda_stream)
     for name, flags, tn, sk, hot in [("full sk", 0, 0, 0, 0), ("nocompute sk", DBG, 0, 0, 0),
                                      ("full cluster", 4, 0, 0, 0), ("nocompute cluster", DBG | 4, 0, 0, 0),
-                                     ("full sk L2-hot", 0, 0, 0, 1), ("nomma sk L2-hot", 1 << 27, 0, 0, 1)]:
+                                     ("nomma sk", 1 << 27, 0, 0, 0), ("nosttm sk", 1 << 25, 0, 0, 0),
+                                     ("full sk L2-hot", 0, 0, 0, 1), ("nomma sk L2-hot", 1 << 27, 0, 0, 1),
+                                     ("nosttm sk L2-hot", 1 << 25, 0, 0, 1), ("nocompute sk L2-hot", DBG, 0, 0, 1)]:
         if hot and wb > 60e6:
             continue   # does not stay in L2
         us = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[0 if hot else i % R].data_ptr(), M, N,
