@@ -1193,6 +1193,32 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
     if (2 * (U / P) >= NA && (NA <= kMaxAccumK / quick::kKA || (U + P - 1) / P <= kMaxAccumK / quick::kKA))
       return Plan{tn, 1, (int)P, true, (int)P};
   }
+  const int s_min = (K + kMaxAccumK - 1) / kMaxAccumK;
+  if (force_tile == 0 && force_split == 0 && M > 128) {
+    // Large M (tensor-bound): cost model over tile in {128, 256} tokens and split S, in cycles
+    // per SM: waves x (A stages per CTA x stage time + fixed per-CTA cost).  Measured stage
+    // times on B200 (tools/trace_gemm.py): 128 x 128 tokens ~700 cycles (8 MMAs of 512 + issue
+    // gaps), 128 x 256 tokens ~1280 (MMA pipe ~80 % busy); ~7000 cycles of prologue/epilogue
+    // per CTA, +2000 for a DSMEM split-K reduce.  Waves count resident clusters (GPC placement).
+    double best = 1e300;
+    Plan bp{128, 1, 0, false, 0};
+    for (int tc : {128, 256}) {
+      const int tl = (N / quick::kTileRows) * ((M + tc - 1) / tc);
+      const double stage = tc == 256 ? 1280.0 : 700.0;
+      for (int s2 = 1; s2 <= quick::kMaxSplit; ++s2) {
+        if (s2 < s_min) continue;
+        if (s2 > 1 && s2 > NA / 2) break;
+        const int res = max_resident(tc, false, s2);
+        const long long waves = ((long long)tl + res - 1) / res;
+        const double t = (double)waves * (((NA + s2 - 1) / s2) * stage + 7000.0 + (s2 > 1 ? 2000.0 : 0.0));
+        if (t < best) {
+          best = t;
+          bp = Plan{tc, s2, tl * s2, false, 0};
+        }
+      }
+    }
+    return bp;
+  }
   int S = 1;
   if (force_split > 0) {
     S = force_split;
@@ -1203,7 +1229,6 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
       if (tiles > max_resident(tn, false, s2)) continue;
       S = s2;
     }
-    const int s_min = (K + kMaxAccumK - 1) / kMaxAccumK;
     if (S < s_min) S = std::min(s_min, quick::kMaxSplit);
   }
   return Plan{tn, S, tiles * S, false, 0};

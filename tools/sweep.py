@@ -70,14 +70,20 @@ for (N, K) in SHAPES[which]:
         F = 2 * M * N * K
         rec = {"N": N, "K": K, "M": M, "plan": quick.quick_gemm_plan(M, N, K, G)}
         for mode in modes:
-            fl = FLAGS[mode]
+            # "auto" / "pdl" / "nosk", or a forced plan "t<tile>s<split>" (e.g. t256s2)
+            fl, tn, sk = FLAGS.get(mode, 0), 0, 0
+            if mode.startswith("t"):
+                tn, sk = (int(v) for v in mode[1:].split("s"))
+                if tn > 2 * M and tn > 16:
+                    continue
             us = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
-                                                              y.data_ptr(), stream.cuda_stream, fl))
+                                                              y.data_ptr(), stream.cuda_stream, fl, tn, sk))
             rec[mode] = {"us": round(us, 3), "hbm": round(B / (us * 1e-6) / HBM, 4),
                          "tc": round(F / (us * 1e-6) / TC, 4)}
         f.write(json.dumps(rec) + "\n")
         f.flush()
         print(N, K, M, rec["plan"], " ".join("%s %.2fus hbm %.3f tc %.3f" % (m, rec[m]["us"], rec[m]["hbm"],
-                                                                            rec[m]["tc"]) for m in modes), flush=True)
+                                                                            rec[m]["tc"]) for m in modes if m in rec),
+              flush=True)
     del copies, blob
     torch.cuda.empty_cache()
