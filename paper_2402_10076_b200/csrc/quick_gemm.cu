@@ -90,7 +90,7 @@ struct Cfg {
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
   static constexpr int STAGES = NPAR == 4 ? (BN <= 16 ? 8 : BN <= 32 ? 6 : 8)
-                                          : (BN <= 128 ? 4 : 3);
+                                          : (BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 128 ? 4 : 3);
   static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
@@ -788,7 +788,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
     // ---------------------------------------------------------------- cluster split-K reduce
     // fixed order p = 0..S-1 over the cluster's fp32 partials: deterministic (reading R12).
     // All S DSMEM loads of an element are issued before the first add (latency ~200 cycles).
+    if (TRACE && tr != nullptr && threadIdx.x == 0) tr[5] = clock64();
     ptx::cluster_sync();
+    if (TRACE && tr != nullptr && threadIdx.x == 0) tr[6] = clock64();
     const int m0 = blockIdx.z * BN;
     const uint32_t my = ptx::cluster_ctarank();
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
@@ -826,6 +828,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
       }
     }
+    if (TRACE && tr != nullptr && threadIdx.x == 0) tr[7] = clock64();
     ptx::cluster_sync();   // peers may still be reading our partials
   }
 

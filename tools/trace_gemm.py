@@ -62,7 +62,9 @@ for c in range(16):
     nst = int(row[3])
     n = min(nst, TS)
     ev = row[8:].reshape(7, TS)[:, :n].astype(np.int64) - int(row[0])
-    print(f"CTA {c} sm {row[4]} nst {nst}: setup->end {int(row[2]) - int(row[0])} cyc, dfull at {int(row[1]) - int(row[0])}")
+    print(f"CTA {c} sm {row[4]} nst {nst}: setup->end {int(row[2]) - int(row[0])} cyc, dfull at {int(row[1]) - int(row[0])}"
+          + (f", split-K: partials stored {int(row[5]) - int(row[0])}, cluster sync 1 {int(row[6]) - int(row[0])},"
+             f" reduced {int(row[7]) - int(row[0])}" if row[5] else ""))
     if c < 2:
         for i in list(range(min(n, 6))) + list(range(max(6, n - 3), n)):
             print("  it", i, " ".join(f"{nm}={ev[j, i]}" for j, nm in enumerate(names)))
