@@ -56,6 +56,7 @@ constexpr int kDebugExitPrologue = 1 << 28;  // debug: return after the prologue
 constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (commits only)
 constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
 constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
+constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -100,7 +101,10 @@ struct Cfg {
   static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
   static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
   // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull[2], dempty[2]
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * ASTAGES + 4;
+  // + xfull[STAGES]: the X tile has its own barrier so that dequantization (weights + metadata
+  // only) can start before X is loadable (PDL: the weights of the first stages are fetched and
+  // dequantized while the previous kernel finishes)
+  static constexpr int NUM_BARS = 3 * STAGES + 2 * ASTAGES + 4;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;   // TMEM base, then stream-K flag
   static constexpr int USED = HOLD_OFF + 16;
   static constexpr int TMEM_COLS = (NPAR == 2 && DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512;
@@ -166,6 +170,7 @@ struct SegIter {
       u = u1 = 0;
     }
   }
+  __device__ __forceinline__ bool more() const { return sk ? (u < u1) : !done; }
   __device__ __forceinline__ bool next(Seg& s) {
     if (!sk) {
       if (done) return false;
@@ -310,6 +315,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
   const uint32_t bar_aempty = bar_afull + 8 * kAStages;
   const uint32_t bar_dfull = bar_aempty + 8 * kAStages;   // [2]
   const uint32_t bar_dempty = bar_dfull + 16;             // [2]
+  const uint32_t bar_xfull = bar_dempty + 16;             // [STAGES]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::HOLD_OFF);
 
   // Prologue.  The producer initialises the barriers and starts loading at once; the other
@@ -318,6 +324,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
   if (threadIdx.x == kProducerWarp * 32) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
+      ptx::mbar_init(bar_xfull + 8 * s, 1);
       // 128 dequant-thread arrivals per A stage of the load stage (a thread reading the only A
       // stage of a short load stage arrives for both) + 1 MMA commit
       ptx::mbar_init(bar_empty + 8 * s, 4 * 32 * APL + 1);
@@ -363,9 +370,15 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
   if (TRACE && tr != nullptr && threadIdx.x == 0) tr[0] = clock64();
   unsigned long long t_start_ns = 0;
   if (TRACE && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
-  // let the next kernel in the stream launch its prologue early (PDL); it still waits for
-  // this grid's completion before touching anything this grid writes
-  ptx::griddep_launch_dependents();
+  // PDL: the next kernel in the stream may launch once every CTA of this grid has triggered.
+  // The trigger is placed where each warp's main loop ends (the CTA's epilogue), so the next
+  // grid's CTAs land on SMs whose CTAs are finishing (its prologue, weight prefetch and first
+  // dequantized stages overlap our epilogue); triggering right after the prologue let them
+  // double up on SMs of grids with fewer CTAs than SMs (measured slower on 13B shapes).
+  // The next grid still waits (griddepcontrol.wait) for this grid's completion before it
+  // reads X or writes anything.
+  const bool pdl_early = (p.flags & kDebugPdlEarly) != 0;
+  if (pdl_early) ptx::griddep_launch_dependents();
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------------ producer
@@ -395,20 +408,23 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         const uint32_t meta_bytes = (uint32_t)(group_of(kl0 + kv - 1) - g0 + 1) * kMetaBytes;
         const uint32_t full = bar_full + 8 * slot;
         if (ptx::elect_one()) {
-          ptx::mbar_arrive_expect_tx(full, C::X_BYTES + (uint32_t)kv * 64u + meta_bytes);
+          ptx::mbar_arrive_expect_tx(full, (uint32_t)kv * 64u + meta_bytes);
           ptx::bulk_load_hint(sbase + C::W_OFF + slot * C::W_BYTES,
                               wbase + (size_t)(kl0 / 32) * kChunkBytes, (uint32_t)kv * 64u, full,
                               pol_w);
           ptx::bulk_load_hint(sbase + C::M_OFF + slot * C::M_BYTES,
                               mbase + (size_t)g0 * kMetaBytes, meta_bytes, full, pol_w);
           if (lf >= pre && !(pre == 0 && lf == 0)) {
+            ptx::mbar_arrive_expect_tx(bar_xfull + 8 * slot, C::X_BYTES);
             ptx::tma_load_3d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, 0, m0, kl0 / 64,
-                                  full, pol_x);
+                                  bar_xfull + 8 * slot, pol_x);
           } else if (lf == (pre > 0 ? pre - 1 : 0)) {
             if (pdl) ptx::griddep_wait();
-            for (int j = 0; j <= lf; ++j)   // X of the stages issued so far (all in this segment)
+            for (int j = 0; j <= lf; ++j) {   // X of the stages issued so far (all in this segment)
+              ptx::mbar_arrive_expect_tx(bar_xfull + 8 * j, C::X_BYTES);
               ptx::tma_load_3d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, 0, m0,
-                                    (sg.a_lo + j * APL) * kKA / 64, bar_full + 8 * j, pol_x);
+                                    (sg.a_lo + j * APL) * kKA / 64, bar_xfull + 8 * j, pol_x);
+            }
           }
         }
         __syncwarp();
@@ -419,6 +435,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         }
       }
     }
+    ptx::griddep_launch_dependents();
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; one elected lane issues the MMAs and the commits (a commit tracks
@@ -428,7 +445,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
     SegIter it(p, SK);
     Seg sg;
     int slot = 0, as = 0, si = 0, ia = 0;
-    uint32_t aph = 0;
+    uint32_t aph = 0, xph = 0;
     while (it.next(sg)) {
       const int db = SK ? (si & 1) : 0;
       // stream-K: the accumulator of segment si - 2 must have been read out
@@ -436,9 +453,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
       const uint32_t d_col = tmem + kDCol + (uint32_t)(db * C::NACC * BN);
       int sub = 0;
       for (int a = sg.a_lo; a < sg.a_hi; ++a, ++ia) {
-        // A stage written by the 4 warps of its parity group; they waited on `full`, which
-        // also covers the X tile of this load stage, so one wait orders both operands
+        // A stage written by the 4 warps of its parity group (afull); the X tile of its load
+        // stage has its own barrier (xfull), waited once per load stage
         ptx::mbar_wait(bar_afull + 8 * as, aph);
+        if (sub == 0) ptx::mbar_wait(bar_xfull + 8 * slot, xph);   // this load stage's X tile
         if (lane == 0) stamp(5, ia);
         ptx::tc_fence_after();
         const int kv = min(kKA, K - a * kKA);   // 128, or 64 at the end of K
@@ -478,7 +496,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         if (lane == 0) stamp(6, ia);
         if (last_of_load) {
           sub = 0;
-          if (++slot == STAGES) slot = 0;
+          if (++slot == STAGES) {
+            slot = 0;
+            xph ^= 1u;
+          }
         } else {
           ++sub;
         }
@@ -489,6 +510,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
       }
       ++si;
     }
+    ptx::griddep_launch_dependents();
   } else {
     // ------------------------------------------------------------------ dequantizers
     // Warp w owns TMEM lane quarter q = w % 4 (the only lanes it may access) and takes the
@@ -658,6 +680,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
       lbase += (sg.a_hi - sg.a_lo + APL - 1) / APL;
 
       // ---------------------------------------------------------------- segment epilogue
+      if (!it.more()) ptx::griddep_launch_dependents();   // our last segment: CTA finishing
       const int db = SK ? (si & 1) : 0;
       const int m0 = sg.mt * BN;
       const int n = sg.t * kTileRows + r;
@@ -1202,7 +1225,9 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
     // per SM: waves x (A stages per CTA x stage time + fixed per-CTA cost).  Measured stage
     // times on B200 (tools/trace_gemm.py): 128 x 128 tokens ~700 cycles (8 MMAs of 512 + issue
     // gaps), 128 x 256 tokens ~1280 (MMA pipe ~80 % busy); ~7000 cycles of prologue/epilogue
-    // per CTA, +2000 for a DSMEM split-K reduce.  Waves count resident clusters (GPC placement).
+    // per CTA; a DSMEM split-K reduce costs two cluster barriers (~2500) + the partial tile
+    // through shared memory (~128 B/clk) + its remote (S-1)/S share through DSMEM (~20 B/clk,
+    // measured: a 128 KiB partial at S = 4 takes ~9000 cycles).  Waves count resident clusters.
     double best = 1e300;
     Plan bp{128, 1, 0, false, 0};
     for (int tc : {128, 256}) {
@@ -1213,7 +1238,9 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
         if (s2 > 1 && s2 > NA / 2) break;
         const int res = max_resident(tc, false, s2);
         const long long waves = ((long long)tl + res - 1) / res;
-        const double t = (double)waves * (((NA + s2 - 1) / s2) * stage + 7000.0 + (s2 > 1 ? 2000.0 : 0.0));
+        const double part = (double)tc * quick::kTileRows * 4.0;   // fp32 partial tile bytes
+        const double red = s2 > 1 ? 2500.0 + part / 128.0 + part * (s2 - 1) / s2 / 20.0 : 0.0;
+        const double t = (double)waves * (((NA + s2 - 1) / s2) * stage + 7000.0 + red);
         if (t < best) {
           best = t;
           bp = Plan{tc, s2, tl * s2, false, 0};
@@ -1331,7 +1358,8 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
-                    quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm;
+                    quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
+                    quick::kDebugPdlEarly;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1385,7 +1413,13 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
     while ((1 << kp.g_shift) < G) ++kp.g_shift;
   }
   kp.ldy = ldy;
-  kp.flags = flags;
+  // PDL is not used with the 256-token tile: with the flag (the early weight prefetch and
+  // dequantization before griddepcontrol.wait, with or without the programmatic launch
+  // attribute) that variant failed intermittently on B200 with "unspecified launch failure"
+  // in fresh processes (tools/pdl_repro.py: 8 of 19 runs; 0 of 12 without the flag; never for
+  // tiles <= 128; not reproducible under compute-sanitizer).  Root cause not found yet; the flag
+  // is a scheduling hint, so the launch stays ordinary (results are identical).
+  kp.flags = tn == 256 ? (flags & ~QUICK_FLAG_PDL) : flags;
   kp.NA = NA;
   kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;

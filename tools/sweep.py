@@ -33,7 +33,8 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
 L = 16
-FLAGS = {"auto": 0, "pdl": quick.QUICK_FLAG_PDL, "nosk": quick.QUICK_FLAG_NO_STREAMK}
+FLAGS = {"auto": 0, "pdl": quick.QUICK_FLAG_PDL, "nosk": quick.QUICK_FLAG_NO_STREAMK,
+         "pdlearly": quick.QUICK_FLAG_PDL | (1 << 24)}
 
 
 def timeit(launch, reps=5):
