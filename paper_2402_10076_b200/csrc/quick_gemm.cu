@@ -1109,6 +1109,12 @@ int max_resident(int bn, bool sk, int S) {
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
       if (cudaOccupancyMaxActiveClusters(&n, kernel_for(bn, sk), &cfg) != cudaSuccess) n = 0;
+      // like the per-CTA occupancy query, the cluster query assumes one CTA per SM for these
+      // kernels although two co-reside (TMEM <= 256 columns, <= 113 KiB shared memory): take
+      // the per-SM capacity computed above, less 10 % for GPC fragmentation of the clusters
+      // (overestimating only costs a partial second wave: clusters never wait on each other)
+      const int per_sm = max_resident(bn, sk, 1) / std::max(1, sm_count());
+      if (per_sm >= 2) n = std::max(n, (per_sm * sm_count() * 9) / (10 * S));
     }
   }
   cudaGetLastError();  // occupancy queries must not leave a sticky error behind
@@ -1253,12 +1259,19 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
   if (force_split > 0) {
     S = force_split;
   } else {
+    // the largest S <= 6 whose clusters are all resident in one wave, preferring an S that
+    // divides the A stages evenly (the cluster waits for its slowest member: a 5-vs-6-stage
+    // split costs a stage); measured on B200: 4096^2 S=4 (6.0 us) beats S=8 (6.6), 13824x5120
+    // S=2 (13.1) beats S=1 (15.6), 5120x13824 S=6 (13.6) beats S=3 (16.0)
     const int cap = max_resident(tn, false, 1);   // CTAs/SM from TMEM, smem and registers
-    for (int s2 = 2; s2 <= quick::kMaxSplit && s2 <= NA / 2; ++s2) {
+    int s_any = 1, s_div = 1;
+    for (int s2 = 2; s2 <= 6 && s2 <= NA / 2; ++s2) {
       if (tiles * s2 > cap) break;
       if (tiles > max_resident(tn, false, s2)) continue;
-      S = s2;
+      s_any = s2;
+      if (NA % s2 == 0) s_div = s2;
     }
+    S = (2 * s_div >= s_any) ? s_div : s_any;
     if (S < s_min) S = std::min(s_min, quick::kMaxSplit);
   }
   return Plan{tn, S, tiles * S, false, 0};
