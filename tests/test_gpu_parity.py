@@ -233,3 +233,45 @@ def test_full_size_shapes_sampled(M, N, K):
     cols = np.unique(np.concatenate([np.arange(8), np.arange(N - 8, N), rng.choice(N, 240, replace=False)]))
     cols = cols[:len(cols) // 8 * 8]
     _sampled_cols_check(p, y, cols)
+
+
+# ------------------------------------------------------------------------------- PDL
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (16, 13824, 5120), (16, 28672, 1024), (64, 4096, 4096),
+                                   (200, 4096, 4096), (256, 2048, 4096)])
+def test_pdl_chain_matches_ordinary_launches(M, N, K):
+    """QUICK_FLAG_PDL (the bench's launch mode): the second GEMM reads the first one's output as
+    its X and is launched programmatically dependent on it, so its weight prefetch and first
+    dequantized stages overlap GEMM 1, while its X loads must wait for GEMM 1's completion.
+    Chain Y2 = (X . W1) . W2 repeated back to back, eagerly and under CUDA-graph capture; every
+    result must be bit-identical to ordinary launches (covers the cluster split-K, stream-K and
+    wide-tile plans, incl. the 256-token tile where the flag is ignored)."""
+    G = 128
+    p1 = synth.make_problem(M + N, M=M, N=N, K=K, G=G)
+    p2 = synth.make_problem(M + N + 1, M=M, N=K, K=N, G=G)   # K2 = N1: X2 = Y1
+    x, w1, w2 = to_dev_f16(p1.x), pack_dev(p1), pack_dev(p2)
+    y1 = quick.quick_w4a16_gemm(x, w1, N, K, G)
+    y2 = quick.quick_w4a16_gemm(y1, w2, K, N, G)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        a1 = torch.empty_like(y1)
+        a2 = torch.empty_like(y2)
+        for _ in range(3):
+            quick.quick_w4a16_gemm(x, w1, N, K, G, out=a1, pdl=True)
+            quick.quick_w4a16_gemm(a1, w2, K, N, G, out=a2, pdl=True)
+        stream.synchronize()
+        assert torch.equal(a1.view(torch.int16), y1.view(torch.int16))
+        assert torch.equal(a2.view(torch.int16), y2.view(torch.int16))
+        a1.zero_()
+        a2.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(2):
+                quick.quick_w4a16_gemm(x, w1, N, K, G, out=a1, pdl=True)
+                quick.quick_w4a16_gemm(a1, w2, K, N, G, out=a2, pdl=True)
+        g.replay()
+        g.replay()
+        stream.synchronize()
+    assert torch.equal(a1.view(torch.int16), y1.view(torch.int16))
+    assert torch.equal(a2.view(torch.int16), y2.view(torch.int16))
+    check_tol(p1, y1)
