@@ -57,6 +57,7 @@ constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (
 constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
 constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
 constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
+constexpr int kDebugPdl256 = 1 << 23;      // debug: keep QUICK_FLAG_PDL for the 256-token tile
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -1372,7 +1373,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
                     quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly;
+                    quick::kDebugPdlEarly | quick::kDebugPdl256;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1432,7 +1433,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   // in fresh processes (tools/pdl_repro.py: 8 of 19 runs; 0 of 12 without the flag; never for
   // tiles <= 128; not reproducible under compute-sanitizer).  Root cause not found yet; the flag
   // is a scheduling hint, so the launch stays ordinary (results are identical).
-  kp.flags = tn == 256 ? (flags & ~QUICK_FLAG_PDL) : flags;
+  kp.flags = (tn == 256 && !(flags & quick::kDebugPdl256)) ? (flags & ~QUICK_FLAG_PDL) : flags;
   kp.NA = NA;
   kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;
