@@ -453,7 +453,56 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
       if (SK && si >= 2) ptx::mbar_wait(bar_dempty + 8 * db, (uint32_t)(((si >> 1) + 1) & 1));
       const uint32_t d_col = tmem + kDCol + (uint32_t)(db * C::NACC * BN);
       int sub = 0;
+      const bool dbg_skip = dbg_nocompute || (p.flags & (kDebugNoMma | kDebugNoSttm));
       for (int a = sg.a_lo; a < sg.a_hi; ++a, ++ia) {
+        // Paired fast path (2 A stages per load stage, both full, not the segment's first): one
+        // iteration waits both A stages and the X tile, and issues 16 MMAs with one set of
+        // bookkeeping -- the per-stage loop overhead of this warp (~470 cycles measured with
+        // two CTAs per SM) was the small-M bottleneck, not the tensor pipe (~200 cycles).
+        if (APL == 2 && sub == 0 && a + 1 < sg.a_hi && (a + 2) * kKA <= K && a != sg.a_lo) {
+          const int as1 = (as + 1 == kAStages) ? 0 : as + 1;
+          const uint32_t aph1 = (as + 1 == kAStages) ? (aph ^ 1u) : aph;
+          ptx::mbar_wait(bar_afull + 8 * as, aph);
+          ptx::mbar_wait(bar_xfull + 8 * slot, xph);
+          ptx::tc_fence_after();
+          const uint64_t dstage = desc0 + (uint64_t)((slot * C::X_BYTES) >> 4);
+          if (ptx::elect_one()) {
+            if (!dbg_skip) {
+              const uint32_t a_col = tmem + as * kAColsPerStage;
+#pragma unroll
+              for (int kk = 0; kk < kKA / 16; ++kk)
+                ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
+                                    dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
+            }
+            ptx::mma_commit(bar_aempty + 8 * as);
+          }
+          __syncwarp();
+          ptx::mbar_wait(bar_afull + 8 * as1, aph1);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            if (!dbg_skip) {
+              const uint32_t a_col = tmem + as1 * kAColsPerStage;
+              const uint64_t d1 = dstage + (uint64_t)((2 * C::X_SUB) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < kKA / 16; ++kk)
+                ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
+                                    d1 + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
+            }
+            ptx::mma_commit(bar_aempty + 8 * as1);
+            ptx::mma_commit(bar_empty + 8 * slot);
+            if (a + 1 == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
+          }
+          __syncwarp();
+          ++a;
+          ++ia;
+          if (++slot == STAGES) {
+            slot = 0;
+            xph ^= 1u;
+          }
+          as = (as1 + 1 == kAStages) ? 0 : as1 + 1;
+          aph = (as1 + 1 == kAStages) ? (aph1 ^ 1u) : aph1;
+          continue;
+        }
         // A stage written by the 4 warps of its parity group (afull); the X tile of its load
         // stage has its own barrier (xfull), waited once per load stage
         ptx::mbar_wait(bar_afull + 8 * as, aph);
@@ -463,7 +512,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         const int kv = min(kKA, K - a * kKA);   // 128, or 64 at the end of K
         const bool last_of_load = (sub == APL - 1) || (a == sg.a_hi - 1);
         if (ptx::elect_one()) {
-          if (dbg_nocompute || (p.flags & (kDebugNoMma | kDebugNoSttm))) {
+          if (dbg_skip) {
             ptx::mma_commit(bar_aempty + 8 * as);
             if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);
             if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
