@@ -49,6 +49,17 @@ if len(rec):
           f"{busy.min():.2f}/{np.median(busy):.2f}/{busy.max():.2f} us, start skew max {(rec[:,1].max()-t0)/1e3:.2f} us")
     full = tt[16 * STRIDE:].reshape(-1, 3)
     idx = np.nonzero(full[:, 1] > 0)[0]
+    # per SM: the CTAs sharing it, by launch index (is the same one always the fast one?)
+    by_sm = {}
+    for i in idx:
+        by_sm.setdefault(int(full[i, 0]), []).append((int(i), (full[i, 2] - full[i, 1]) / 1e3))
+    pairs = [sorted(v) for v in by_sm.values() if len(v) == 2]
+    if pairs:
+        lo = np.array([p[0][1] for p in pairs])
+        hi = np.array([p[1][1] for p in pairs])
+        print(f"SMs with 2 CTAs: {len(pairs)}; lower-index CTA duration mean {lo.mean():.2f} us, higher-index "
+              f"{hi.mean():.2f} us; lower-index faster on {int((lo < hi).sum())} SMs; index gap "
+              f"{np.mean([p[1][0] - p[0][0] for p in pairs]):.1f}")
     d_all = (full[idx, 2] - full[idx, 1]) / 1e3
     slow = idx[d_all > 2 * np.median(d_all)]
     print("slow CTAs (lin idx, smid, start us, dur us):",
