@@ -78,8 +78,8 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
                                 kernel in the stream; X is read and Y written only after that
                                 kernel completes.  The weights must not be written by the
                                 immediately preceding kernel.  The first weight stages are
-                                also dequantized before that point.  Ignored (ordinary launch)
-                                when the plan uses the 256-token tile. */
+                                also dequantized before that point (one stage only for the
+                                256-token tile). */
 #define QUICK_FLAG_NO_STREAMK 4 /* never use the stream-K schedule (tests / A-B timing) */
 
 /* Extended form used by tensor parallelism, layer stacks and the tests.

@@ -57,7 +57,6 @@ constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (
 constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
 constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
 constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
-constexpr int kDebugPdl256 = 1 << 23;      // debug: keep QUICK_FLAG_PDL for the 256-token tile
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -400,6 +399,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
       const int k_seg_end = min(sg.a_hi * kKA, K);
       const int nl = (sg.a_hi - sg.a_lo + APL - 1) / APL;
       if (pre < 0) pre = pdl ? (nl < STAGES ? nl : STAGES) : 0;
+      // The 256-token tile prefetches only one stage ahead of X: with its weights for 2-3 load
+      // stages issued before the first X tile, it failed intermittently with "unspecified
+      // launch failure" (tools/pdl_repro.py on B200: pre 3 -> 5 of 6 runs, pre 2 -> 2 of 5,
+      // pre 1 -> 0 of 5; never for tiles <= 128).  Root cause not identified.
+      if (BN == 256 && pre > 1) pre = 1;
       for (int l = 0; l < nl; ++l, ++lf) {
         const int kl0 = (sg.a_lo + l * APL) * kKA;
         const int kv = min(C::KL, k_seg_end - kl0);   // valid k in this load stage
@@ -1422,7 +1426,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
                     quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly | quick::kDebugPdl256;
+                    quick::kDebugPdlEarly;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1476,13 +1480,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
     while ((1 << kp.g_shift) < G) ++kp.g_shift;
   }
   kp.ldy = ldy;
-  // PDL is not used with the 256-token tile: with the flag (the early weight prefetch and
-  // dequantization before griddepcontrol.wait, with or without the programmatic launch
-  // attribute) that variant failed intermittently on B200 with "unspecified launch failure"
-  // in fresh processes (tools/pdl_repro.py: 8 of 19 runs; 0 of 12 without the flag; never for
-  // tiles <= 128; not reproducible under compute-sanitizer).  Root cause not found yet; the flag
-  // is a scheduling hint, so the launch stays ordinary (results are identical).
-  kp.flags = (tn == 256 && !(flags & quick::kDebugPdl256)) ? (flags & ~QUICK_FLAG_PDL) : flags;
+  kp.flags = flags;
   kp.NA = NA;
   kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;
