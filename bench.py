@@ -344,28 +344,77 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
     xd = [g["xs"][0] for g in gemms]
     sh = stream.cuda_stream
 
+    pipelined = world == 1
+    if pipelined:
+        # copies overlap the GEMMs, as a serving loop would run them: X uploads on one copy
+        # stream, Y downloads on another, the GEMMs on `stream`; per-GEMM buffers and events
+        # order each GEMM after its upload and each download after its GEMM, and an upload /
+        # GEMM waits for the previous step's use of its buffer
+        s_h2d, s_d2h = torch.cuda.Stream(stream.device), torch.cuda.Stream(stream.device)
+        ev = {k: [torch.cuda.Event() for _ in gemms] for k in ("h2d", "comp", "d2h")}
+        started = [False] * len(gemms)
+
     def step(i):
         for gi, g in enumerate(gemms):
-            xd[gi].copy_(xh[gi], non_blocking=True)
             slot = (i * len(gemms) + gi) % R
+            if not pipelined:
+                xd[gi].copy_(xh[gi], non_blocking=True)
+                quick.quick_w4a16_gemm_raw(xd[gi].data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nr"],
+                                           g["K"], G, g["y"].data_ptr(), sh)
+                if world > 1:
+                    collective(g)
+                    yh[gi].copy_(g["yfull"], non_blocking=True)
+                else:
+                    yh[gi].copy_(g["y"], non_blocking=True)
+                continue
+            with torch.cuda.stream(s_h2d):
+                if started[gi]:
+                    s_h2d.wait_event(ev["comp"][gi])      # the previous GEMM on xd[gi] is done
+                xd[gi].copy_(xh[gi], non_blocking=True)
+                ev["h2d"][gi].record(s_h2d)
+            stream.wait_event(ev["h2d"][gi])
+            if started[gi]:
+                stream.wait_event(ev["d2h"][gi])          # y[gi] has been read back
             quick.quick_w4a16_gemm_raw(xd[gi].data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nr"],
                                        g["K"], G, g["y"].data_ptr(), sh)
-            if world > 1:
-                collective(g)
-                yh[gi].copy_(g["yfull"], non_blocking=True)
-            else:
+            ev["comp"][gi].record(stream)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev["comp"][gi])
                 yh[gi].copy_(g["y"], non_blocking=True)
+                ev["d2h"][gi].record(s_d2h)
+            started[gi] = True
 
     for i in range(3):
         step(i)
     torch.cuda.synchronize()
+    graph = None
+    if pipelined:
+        # one step = one CUDA-graph replay: the 9 uploads, GEMMs (C-ABI calls, captured) and
+        # read-backs with their cross-stream event edges, forked from and joined to `stream`
+        # (replays on `stream` are ordered, so buffers are reused safely across steps)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            s_h2d.wait_event(fork)
+            s_d2h.wait_event(fork)
+            started[:] = [False] * len(gemms)
+            step(0)
+            for gi in range(len(gemms)):
+                stream.wait_event(ev["d2h"][gi])
+            stream.wait_event(ev["h2d"][len(gemms) - 1])
+        graph.replay()
+        torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for i in range(steps):
-        step(i)
+        if graph is not None:
+            graph.replay()
+        else:
+            step(i)
     b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
@@ -378,7 +427,10 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
             "h2d_bytes_per_step": int(sum(2 * g["M"] * g["K"] for g in gemms)),
             "d2h_bytes_per_step": int(sum(2 * g["M"] * g["N"] for g in gemms)),
             "steps": steps, "ms_per_step": round(ms / steps, 4),
-            "path": "C-ABI quick_w4a16_gemm per GEMM, eager (no graph), pinned H2D X + D2H Y each step"}
+            "path": ("C-ABI quick_w4a16_gemm per GEMM, pinned H2D X + D2H Y each step"
+                     + ("; one CUDA-graph replay per step holding the uploads, the captured C-ABI GEMM calls and "
+                        "the read-backs on three streams with event dependencies (copies overlap GEMMs)"
+                        if world == 1 else ""))}
 
 
 # ------------------------------------------------------------------------------------------ CPU arm
