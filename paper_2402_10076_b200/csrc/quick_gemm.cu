@@ -463,9 +463,12 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         // iteration waits both A stages and the X tile, and issues 16 MMAs with one set of
         // bookkeeping -- the per-stage loop overhead of this warp (~470 cycles measured with
         // two CTAs per SM) was the small-M bottleneck, not the tensor pipe (~200 cycles).
-        if (APL == 2 && sub == 0 && a + 1 < sg.a_hi && (a + 2) * kKA <= K && a != sg.a_lo) {
+        // (APL == 1: the two A stages are consecutive load stages with their own X slots)
+        if (sub == 0 && a + 1 < sg.a_hi && (a + 2) * kKA <= K && a != sg.a_lo) {
           const int as1 = (as + 1 == kAStages) ? 0 : as + 1;
           const uint32_t aph1 = (as + 1 == kAStages) ? (aph ^ 1u) : aph;
+          const int slot1 = APL == 2 ? slot : (slot + 1 == STAGES ? 0 : slot + 1);
+          const uint32_t xph1 = (APL == 1 && slot + 1 == STAGES) ? (xph ^ 1u) : xph;
           ptx::mbar_wait(bar_afull + 8 * as, aph);
           ptx::mbar_wait(bar_xfull + 8 * slot, xph);
           ptx::tc_fence_after();
@@ -479,26 +482,31 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
                                     dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
             }
             ptx::mma_commit(bar_aempty + 8 * as);
+            if (APL == 1) ptx::mma_commit(bar_empty + 8 * slot);
           }
           __syncwarp();
           ptx::mbar_wait(bar_afull + 8 * as1, aph1);
+          if (APL == 1) ptx::mbar_wait(bar_xfull + 8 * slot1, xph1);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
             if (!dbg_skip) {
               const uint32_t a_col = tmem + as1 * kAColsPerStage;
-              const uint64_t d1 = dstage + (uint64_t)((2 * C::X_SUB) >> 4);
+              const uint64_t d1 = APL == 2 ? dstage + (uint64_t)((2 * C::X_SUB) >> 4)
+                                           : desc0 + (uint64_t)((slot1 * C::X_BYTES) >> 4);
 #pragma unroll
               for (int kk = 0; kk < kKA / 16; ++kk)
                 ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
                                     d1 + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
             }
             ptx::mma_commit(bar_aempty + 8 * as1);
-            ptx::mma_commit(bar_empty + 8 * slot);
+            ptx::mma_commit(bar_empty + 8 * slot1);
             if (a + 1 == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
           }
           __syncwarp();
           ++a;
           ++ia;
+          slot = slot1;
+          xph = xph1;
           if (++slot == STAGES) {
             slot = 0;
             xph ^= 1u;
