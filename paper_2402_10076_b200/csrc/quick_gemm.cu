@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
     SegIter it(p, SK);
     Seg sg;
-    int slot = 0, as = 0, si = 0, ia = 0;
+    int slot = 0, as = 0, si = 0, ia = 0, lf_mma = 0;
     uint32_t aph = 0, xph = 0;
     while (it.next(sg)) {
       const int db = SK ? (si & 1) : 0;
@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
           __syncwarp();
           ++a;
           ++ia;
+          lf_mma += (APL == 1) ? 2 : 1;
           slot = slot1;
           xph = xph1;
           if (++slot == STAGES) {
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         if (lane == 0) stamp(6, ia);
         if (last_of_load) {
           sub = 0;
+          ++lf_mma;
           if (++slot == STAGES) {
             slot = 0;
             xph ^= 1u;
@@ -571,6 +573,18 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
         }
       }
       ++si;
+    }
+    // Drain: the mbarrier arrivals of this warp's last tcgen05.commits (A-ring and load-ring
+    // slots) must have landed before the CTA exits -- a late arrival would hit the shared
+    // memory of the next CTA placed on this SM (a later wave, or the next kernel under PDL).
+    // Slot s of a ring of R slots received ceil((n - s) / R) commits for n stages in total.
+    for (int s2 = 0; s2 < kAStages; ++s2) {
+      const int n = (ia - s2 + kAStages - 1) / kAStages;
+      if (n > 0) ptx::mbar_wait(bar_aempty + 8 * s2, (uint32_t)((n - 1) & 1));
+    }
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      const int n = (lf_mma - s2 + STAGES - 1) / STAGES;
+      if (n > 0) ptx::mbar_wait(bar_empty + 8 * s2, (uint32_t)((n - 1) & 1));
     }
     ptx::griddep_launch_dependents();
   } else {
