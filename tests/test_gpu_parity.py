@@ -275,3 +275,45 @@ def test_pdl_chain_matches_ordinary_launches(M, N, K):
     assert torch.equal(a1.view(torch.int16), y1.view(torch.int16))
     assert torch.equal(a2.view(torch.int16), y2.view(torch.int16))
     check_tol(p1, y1)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 28672, 8192), (512, 5120, 13824)])
+def test_pdl_wide_tile_multiwave_stress(M, N, K):
+    """The 256-token tile on multi-wave grids under back-to-back PDL launches (the configuration
+    whose deeper weight prefetch failed intermittently): 24 launches, each
+    bit-identical to an ordinary launch."""
+    G = 128
+    p = synth.make_problem(M ^ K, M=M, N=N, K=K, G=G)
+    assert quick.quick_gemm_plan(M, N, K, G)["tile_n"] == 256
+    x, w = to_dev_f16(p.x), pack_dev(p)
+    ref = quick.quick_w4a16_gemm(x, w, N, K, G)
+    torch.cuda.synchronize()
+    outs = [torch.empty_like(ref) for _ in range(3)]
+    for i in range(24):
+        quick.quick_w4a16_gemm(x, w, N, K, G, out=outs[i % 3], pdl=True)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
+
+
+@pytest.mark.parametrize("N,K", [(4096, 4096), (13824, 5120), (5120, 13824), (28672, 8192), (8192, 28672)])
+def test_plans_for_the_baseline_shapes(N, K):
+    """The automatic plan over the BJ shapes and M sweep: a legal tile covering the tokens (or 128/256
+    for large M), split-K keeping every accumulator within 8192 of K (reading R15), at most one wave
+    of resident CTAs for the small tiles."""
+    G = 128
+    NA = K // 128
+    for M in (1, 2, 8, 16, 17, 32, 33, 64, 65, 128, 192, 256, 512, 1024):
+        pl = quick.quick_gemm_plan(M, N, K, G)
+        tn, s, ctas = pl["tile_n"], pl["split_k"], pl["num_ctas"]
+        assert tn in (16, 32, 64, 128, 256)
+        if M <= 64:
+            assert tn >= M and tn <= 64, (M, pl)
+            assert ctas <= 2 * 148, (M, pl)
+        else:
+            assert tn >= 128, (M, pl)
+        if s == 0:   # stream-K: a CTA's share of units never spans more than 64 A stages of one tile
+            tiles = (N // 128) * ((M + tn - 1) // tn)
+            assert -(-tiles * NA // ctas) <= max(64, NA) or NA <= 64
+        else:
+            assert -(-NA // s) <= 64, (M, pl)
