@@ -41,7 +41,7 @@ WORKLOADS = {
     "tiny": (0, [(256, 512)], [8], 128),
 }
 METRIC = "W4A16 GEMM TFLOP/s & HBM GB/s vs roofline, M=1–1024, 1/2/4/8 B200"
-BLOCK_C = 8  # steps per graph replay (M-major)
+BLOCK_C = 32  # steps per graph replay (M-major): PDL overlaps consecutive launches inside a graph
 
 
 def algo_bytes(M, N, K, G):
@@ -323,7 +323,7 @@ def run_quick(args, rank, world, dist):
                    "l2": (f"rotating {R} weight copies ({R * blob_bytes / 2**20:.0f} MiB) > L2 {l2 / 2**20:.0f} MiB; "
                           "every launch reads its weights from HBM") if l2_cold else
                          f"weights L2-resident ({R} copies of {blob_bytes} B < 2.5 x L2)",
-                   "timing": f"CUDA-graph replays of {BLOCK_C} launches per M point, M-major; events between replays",
+                   "timing": f"CUDA-graph replays of {BLOCK_C} launches per M point (PDL between consecutive launches), M-major; events between replays",
                    "launch": "quick_w4a16_gemm_ex with QUICK_FLAG_PDL (programmatic dependent launch), automatic plan"},
         "hbm_gbs_aggregate": round(gbs_all, 1),
         "gpu_launches": K_steps * per_step_launches * (2 if world > 1 else 1),
