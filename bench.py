@@ -39,6 +39,9 @@ WORKLOADS = {
     "llama2_13b_mlp": (2, [(13824, 5120), (5120, 13824)], [1, 2, 4, 8, 16, 32, 64, 128, 256, 512], 128),
     "llama2_70b_mlp": (3, [(28672, 8192)], [1, 16, 64, 128, 256, 512, 1024], 128),
     "tiny": (0, [(256, 512)], [8], 128),
+    # BASELINE.json configs[4]: one Mistral-7B decoder layer's linear stack (QKV, O, gate_up, down);
+    # tokens/s = M / (32 layers x the 4 GEMMs' time); attention, norms and SiLU are not on the path
+    "mistral7b_stack": (4, [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)], [1, 16, 64, 256], 128),
 }
 METRIC = "W4A16 GEMM TFLOP/s & HBM GB/s vs roofline, M=1–1024, 1/2/4/8 B200"
 BLOCK_C = 32  # steps per graph replay (M-major): PDL overlaps consecutive launches inside a graph
@@ -290,6 +293,14 @@ def run_quick(args, rank, world, dist):
                       "bound": "tensor" if fl / by >= ridge else "hbm",
                       "tile_n": g["plan"]["tile_n"], "split_k": g["plan"]["split_k"],
                       "ctas": g["plan"]["num_ctas"]})
+    layer_stack = None
+    if args.workload == "mistral7b_stack":
+        # per batch size: the 4 GEMMs of one layer back to back, x 32 layers
+        layer_stack = []
+        for M in Ms:
+            us_layer = sum(e["us"] for e in sweep if e["M"] == M)
+            layer_stack.append({"M": M, "us_per_layer": round(us_layer, 3),
+                                "tokens_per_s": round(M / (32 * us_layer * 1e-6), 1)})
     dom = max(range(len(gemms)), key=lambda i: per_gemm_ms[i])
     d = sweep[dom]
     if d["bound"] == "tensor":
@@ -329,6 +340,7 @@ def run_quick(args, rank, world, dist):
         "gpu_launches": K_steps * per_step_launches * (2 if world > 1 else 1),
         "roofline": roof,
         "sweep": sweep,
+        **({"layer_stack_32_layers": layer_stack} if layer_stack else {}),
         "e2e": e2e,
         "pack": {"host_seconds": round(pack_s, 4), "bytes": int(sum(b.size for b in blobs))},
         "clocks": sampler.summary(),

@@ -225,7 +225,9 @@ def _sampled_cols_check(p, y, cols):
 
 
 @pytest.mark.parametrize("M,N,K", [(16, 13824, 5120), (512, 5120, 13824), (64, 28672, 8192),
-                                   (1024, 28672, 8192), (256, 8192, 28672)])
+                                   (1024, 28672, 8192), (256, 8192, 28672),
+                                   # BASELINE.json configs[4]: Mistral-7B QKV, O, gate_up, down
+                                   (1, 6144, 4096), (256, 4096, 4096), (16, 28672, 4096), (64, 4096, 14336)])
 def test_full_size_shapes_sampled(M, N, K):
     p = synth.make_problem(M + N, M=M, N=N, K=K, G=128)
     y = run(p)
@@ -317,3 +319,50 @@ def test_plans_for_the_baseline_shapes(N, K):
             assert -(-tiles * NA // ctas) <= max(64, NA) or NA <= 64
         else:
             assert -(-NA // s) <= 64, (M, pl)
+
+
+@pytest.mark.parametrize("M", [1, 64, 256])
+def test_mistral_layer_stack_pdl(M):
+    """BASELINE.json configs[4]: one Mistral-7B decoder layer's linear stack (QKV 6144x4096,
+    O 4096x4096, gate_up 28672x4096, down 4096x14336) launched back to back with PDL in a CUDA
+    graph, down fed from the first 14336 columns of gate_up's output: bit-identical to ordinary
+    launches, and the first output within tolerance of the oracle on sampled columns."""
+    G = 128
+    shapes = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
+    probs = [synth.make_problem(100 + i + M, M=M, N=N, K=K, G=G) for i, (N, K) in enumerate(shapes)]
+    ws = [pack_dev(p) for p in probs]
+    xq, xo = to_dev_f16(probs[0].x), to_dev_f16(probs[1].x)
+    xg = to_dev_f16(probs[2].x)
+
+    def layer(pdl, outs):
+        quick.quick_w4a16_gemm(xq, ws[0], 6144, 4096, G, out=outs[0], pdl=pdl)
+        quick.quick_w4a16_gemm(xo, ws[1], 4096, 4096, G, out=outs[1], pdl=pdl)
+        quick.quick_w4a16_gemm(xg, ws[2], 28672, 4096, G, out=outs[2], pdl=pdl)
+        outs[3].copy_(outs[2][:, :14336])
+        quick.quick_w4a16_gemm(outs[3], ws[3], 4096, 14336, G, out=outs[4], pdl=pdl)
+
+    def bufs():
+        return [torch.empty((M, 6144), device=DEV, dtype=torch.float16),
+                torch.empty((M, 4096), device=DEV, dtype=torch.float16),
+                torch.empty((M, 28672), device=DEV, dtype=torch.float16),
+                torch.empty((M, 14336), device=DEV, dtype=torch.float16),
+                torch.empty((M, 4096), device=DEV, dtype=torch.float16)]
+
+    ref = bufs()
+    layer(False, ref)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    out = bufs()
+    with torch.cuda.stream(stream):
+        layer(True, out)   # eager first (workspace outside capture)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            layer(True, out)
+        for _ in range(3):
+            g.replay()
+        stream.synchronize()
+    for a, b in zip(out, ref):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    cols = np.arange(0, 6144, 97)[: 56]
+    _sampled_cols_check(probs[0], ref[0], cols)
