@@ -39,9 +39,8 @@
 
 namespace quick {
 
-// CTA shape per config (Cfg::NPAR dequant groups of 4 warps, one per TMEM lane quarter, then
-// the producer warp and the MMA warp on the top warp ids)
-constexpr int kMaxThreads = 18 * 32;
+// CTA shape per config: Cfg::NPAR dequant groups of 4 warps (one per TMEM lane quarter), then
+// the producer warp and the MMA warp on the top warp ids
 constexpr int kTileRows = 128;    // weight rows (output columns n) per tile = TMEM lanes
 constexpr int kKA = 128;          // k per A stage (one TMEM A slot, 8 MMAs of K = 16)
 constexpr int kAColsPerStage = kKA / 2;           // 128 fp16 of k = 64 x 32-bit TMEM columns
