@@ -927,7 +927,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
       }
     }
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[7] = clock64();
-    ptx::cluster_sync();   // peers may still be reading our partials
+    // peers may still be reading our partials: arrive now (our own DSMEM reads are done), wait
+    // only at the very end, so the barrier latency overlaps the teardown
+    ptx::cluster_arrive();
   }
 
   ptx::tc_fence_before();
@@ -959,6 +961,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, C::TMEM_COLS);
   }
+  if (!SK && S > 1) ptx::cluster_wait();   // (arrived after the split-K reduce)
 }
 
 // ------------------------------------------------------------------------------------------
