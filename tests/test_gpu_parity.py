@@ -131,6 +131,17 @@ def test_group_sizes(G):
     check_tol(p, run(p, tile_n=128))
 
 
+@pytest.mark.parametrize("M,K", [(16, 512), (5, 1536), (300, 1024)])
+def test_per_channel_groups(M, K):
+    """G = K (one scale and zero per output column): power-of-two and general K,
+    every plan family."""
+    p = synth.make_problem(K + M, M=M, N=384, K=K, G=K)
+    check_tol(p, run(p))
+    check_tol(p, run(p, no_streamk=True))
+    check_tol(p, run(p, split_k=2))
+    check_tol(p, run(p, tile_n=256 if M > 128 else 64))
+
+
 @pytest.mark.parametrize("M", [1, 2, 4, 8, 16, 32, 64, 128, 256])
 def test_llama7b_attention_sweep(M):
     """BASELINE.json configs[1]: N = K = 4096, g128, full-output parity."""
