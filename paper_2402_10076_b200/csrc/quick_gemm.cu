@@ -56,6 +56,7 @@ constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (
 constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
 constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
 constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
+constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memory (Cfg AM = 1)
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -66,7 +67,11 @@ constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the
 //          (stream-K double-buffers D so a segment's epilogue overlaps the next segment's MMAs;
 //          small tiles alternate the K=16 MMAs over NACC = 2 accumulators, summed in the
 //          epilogue, because a single accumulator chain makes N=16 MMAs latency-bound)
-template <int BN, bool SK>
+// AM (A-operand placement): 0 = the dequantized A stage in TMEM (tcgen05.st, TS MMA: the design);
+// 1 = ablation of the paper's Fig. 2 baseline on B200: the dequantized A stage written back to
+// shared memory (STS.128 in the UMMA SWIZZLE_128B K-major layout, conflict-free) and read by an SS
+// MMA (tiles 16 and 128, cluster split-K plans only)
+template <int BN, bool SK, int AM = 0>
 struct Cfg {
   // NPAR dequant groups of 4 warps.  NPAR = 4 (one CTA per SM, 16 dequant warps, the whole TMEM
   // for a 6-7 slot A ring) was measured 1.9x slower per SM than two 2-group CTAs per SM on the
@@ -83,14 +88,14 @@ struct Cfg {
   static constexpr int ASTAGES =
       NPAR == 4 ? (ASTAGES_FIT > 7 ? 7 : ASTAGES_FIT)
                 : (BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2));
-  static constexpr int DCOL = ASTAGES * kAColsPerStage;
+  static constexpr int DCOL = AM == 0 ? ASTAGES * kAColsPerStage : 0;   // A ring columns in TMEM
   static constexpr int NACC = (BN <= 32 && DCOL + NDBUF * 2 * BN <= TMEM_BUDGET) ? 2 : 1;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
   static constexpr int STAGES = NPAR == 4 ? (BN <= 16 ? 8 : BN <= 32 ? 6 : 8)
-                                          : (BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 128 ? 4 : 3);
+                                          : (BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 128 ? (AM ? 3 : 4) : 3);
   static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
@@ -98,7 +103,9 @@ struct Cfg {
   static constexpr int X_OFF = 0;
   static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
   static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
-  static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
+  static constexpr int A_BYTES = kTileRows * kKA * 2;   // AM = 1: one A stage in shared memory
+  static constexpr int A_OFF = (M_OFF + STAGES * M_BYTES + 1023) & ~1023;
+  static constexpr int BAR_OFF = AM == 0 ? ((M_OFF + STAGES * M_BYTES + 7) & ~7) : (A_OFF + ASTAGES * A_BYTES);
   // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull[2], dempty[2]
   // + xfull[STAGES]: the X tile has its own barrier so that dequantization (weights + metadata
   // only) can start before X is loadable (PDL: the weights of the first stages are fetched and
@@ -106,10 +113,12 @@ struct Cfg {
   static constexpr int NUM_BARS = 3 * STAGES + 2 * ASTAGES + 4;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;   // TMEM base, then stream-K flag
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = (NPAR == 2 && DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = AM == 1 ? (NDBUF * NACC * BN <= 32 ? 32 : NDBUF * NACC * BN <= 64 ? 64
+                                                : NDBUF * NACC * BN <= 128 ? 128 : 256)
+                                   : ((NPAR == 2 && DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512);
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
-  static constexpr int MAX_CTAS_PER_SM = 512 / TMEM_COLS;
+  static constexpr int MAX_CTAS_PER_SM = AM == 1 ? 1 : 512 / TMEM_COLS;
   static constexpr int MIN_SMEM = (228 * 1024) / (MAX_CTAS_PER_SM + 1) + 1024;
   static constexpr int SMEM_BYTES = (USED + 1024 > MIN_SMEM ? USED + 1024 : MIN_SMEM);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
@@ -274,11 +283,11 @@ __device__ __forceinline__ constexpr uint32_t instr_desc() {
   return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
 }
 
-template <int BN, bool SK, bool GBIG, bool TRACE>
-__global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PER_SM)
+template <int BN, bool SK, bool GBIG, bool TRACE, int AM = 0>
+__global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const __grid_constant__ KParams p) {
-  using C = Cfg<BN, SK>;
+  using C = Cfg<BN, SK, AM>;
   constexpr int kThreads = C::THREADS;
   constexpr int kProducerWarp = C::PRODUCER_WARP;
   constexpr int kMmaWarp = C::MMA_WARP;
@@ -446,6 +455,17 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
     // the async tcgen05 ops of the thread that issues it, so the same lane does both).
     constexpr uint32_t idesc = instr_desc<BN>();
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
+    // AM = 1: the A stage is an SW128 K-major tile in shared memory (two 64-k sub-tiles of 16 KiB)
+    const uint64_t adesc0 = sw128_desc(sbase + (uint32_t)C::A_OFF);
+    // one K=16 MMA of A stage `a_slot`; `a_col` is its TMEM column (AM = 0)
+    auto mma_k = [&](uint32_t d, uint32_t a_col, int a_slot, int kk, uint64_t bdesc, uint32_t acc) {
+      if constexpr (AM == 0) {
+        ptx::mma_f16_ts(d, a_col + kk * 8, bdesc, idesc, acc);
+      } else {
+        ptx::mma_f16_ss(d, adesc0 + (uint64_t)((a_slot * C::A_BYTES + (kk >> 2) * (kTileRows * 128)) >> 4) +
+                               (uint64_t)((kk & 3) * 2), bdesc, idesc, acc);
+      }
+    };
     SegIter it(p, SK);
     Seg sg;
     int slot = 0, as = 0, si = 0, ia = 0, lf_mma = 0;
@@ -477,8 +497,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
               const uint32_t a_col = tmem + as * kAColsPerStage;
 #pragma unroll
               for (int kk = 0; kk < kKA / 16; ++kk)
-                ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
-                                    dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
+                mma_k(d_col + (uint32_t)((kk % C::NACC) * BN), a_col, as, kk,
+                      dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), 1u);
             }
             ptx::mma_commit(bar_aempty + 8 * as);
             if (APL == 1) ptx::mma_commit(bar_empty + 8 * slot);
@@ -494,8 +514,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
                                            : desc0 + (uint64_t)((slot1 * C::X_BYTES) >> 4);
 #pragma unroll
               for (int kk = 0; kk < kKA / 16; ++kk)
-                ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
-                                    d1 + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
+                mma_k(d_col + (uint32_t)((kk % C::NACC) * BN), a_col, as1, kk,
+                      d1 + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), 1u);
             }
             ptx::mma_commit(bar_aempty + 8 * as1);
             ptx::mma_commit(bar_empty + 8 * slot1);
@@ -538,15 +558,15 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
             // slot is held until these complete, so issue latency throttles the dequantizers)
 #pragma unroll
             for (int kk = 0; kk < kKA / 16; ++kk)
-              ptx::mma_f16_ts_acc(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
-                                  dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc);
+              mma_k(d_col + (uint32_t)((kk % C::NACC) * BN), a_col, as, kk,
+                    dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), 1u);
           } else {
 #pragma unroll
             for (int kk = 0; kk < kKA / 16; ++kk) {
               if (kk * 16 < kv)
-                ptx::mma_f16_ts(d_col + (uint32_t)((kk % C::NACC) * BN), a_col + kk * 8,
-                                dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), idesc,
-                                (first && kk < C::NACC) ? 0u : 1u);
+                mma_k(d_col + (uint32_t)((kk % C::NACC) * BN), a_col, as, kk,
+                      dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2),
+                      (first && kk < C::NACC) ? 0u : 1u);
             }
           }
           ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
@@ -705,8 +725,17 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
 #pragma unroll
               for (int i = 0; i < 32; ++i) x ^= a_regs[i];
               if (x == 0x12345679u) ptx::tmem_st_32x32b_x32(acol, a_regs);
+            } else if constexpr (AM == 1) {
+              // ablation: write the stage back to shared memory (SW128 K-major: row r at r x 128 B,
+              // 16-B chunk c at c ^ (r & 7); 8 rows of a quarter-warp hit 8 distinct chunks)
+              const uint32_t arow = sbase + (uint32_t)(C::A_OFF + as * C::A_BYTES) + (uint32_t)r * 128u;
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                ptx::sts128(arow + (uint32_t)((c ^ (r & 7)) << 4), a_regs[4 * c], a_regs[4 * c + 1],
+                            a_regs[4 * c + 2], a_regs[4 * c + 3]);
             } else {
-            ptx::tmem_st_32x32b_x32(acol, a_regs);
+              ptx::tmem_st_32x32b_x32(acol, a_regs);
+            }
             if ((ka + kKA) <= k_seg_end) {   // second half (all but a short last stage)
               DequantConsts cst2, cst3;
               if constexpr (!GBIG) {
@@ -729,13 +758,23 @@ __global__ void __launch_bounds__(Cfg<BN, SK>::THREADS, Cfg<BN, SK>::MAX_CTAS_PE
 #pragma unroll
                 for (int i = 0; i < 32; ++i) x ^= b_regs[i];
                 if (x == 0x12345679u) ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+              } else if constexpr (AM == 1) {
+                const uint32_t arow =
+                    sbase + (uint32_t)(C::A_OFF + as * C::A_BYTES + kTileRows * 128) + (uint32_t)r * 128u;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                  ptx::sts128(arow + (uint32_t)((c ^ (r & 7)) << 4), b_regs[4 * c], b_regs[4 * c + 1],
+                              b_regs[4 * c + 2], b_regs[4 * c + 3]);
               } else {
                 ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
               }
             }
+            if constexpr (AM == 1) {
+              ptx::fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor core
+            } else {
+              ptx::tmem_wait_st();
+              ptx::tc_fence_before();
             }
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
             ptx::mbar_arrive(bar_afull + 8 * as);
             if (tw) stamp(4, iw);
           }
@@ -1391,6 +1430,20 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   // group-size specialisation: a power of two >= 128 (the group index is a shift and an A
   // stage never straddles groups); any other G takes the per-32-k general path
   const bool gbig = kp.G >= quick::kKA && (kp.G & (kp.G - 1)) == 0;
+  if constexpr (!SK && (BN == 16 || BN == 128)) {
+    if (kp.flags & quick::kAblationSmemA) {   // the shared-memory-A ablation
+      using CA = quick::Cfg<BN, false, 1>;
+      auto* ka = gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, false, 1>
+                      : quick::quick_w4a16_tc_kernel<BN, false, false, false, 1>;
+      e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, CA::SMEM_BYTES);
+      if (e != cudaSuccess) return cuda_fail(e);
+      cfg.dynamicSmemBytes = CA::SMEM_BYTES;
+      cfg.blockDim = dim3((unsigned)CA::THREADS, 1, 1);
+      e = cudaLaunchKernelEx(&cfg, ka, tmap, kp);
+      if (e != cudaSuccess) return cuda_fail(e);
+      return QUICK_OK;
+    }
+  }
   if (g_trace != nullptr)
     e = gbig ? cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true, true>, tmap, kp)
              : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, true>, tmap, kp);
@@ -1450,7 +1503,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
                     quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly;
+                    quick::kDebugPdlEarly | quick::kAblationSmemA;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1458,7 +1511,8 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (split_k < 0 || split_k > quick::kMaxSplit || split_k > NA) return QUICK_ERR_UNSUPPORTED;
 
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
-  Plan plan = choose_plan(M, N, K, G, tile_n, split_k, (flags & QUICK_FLAG_NO_STREAMK) == 0);
+  Plan plan = choose_plan(M, N, K, G, tile_n, split_k,
+                          (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0);
   if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
   quick::KParams kp;
   std::memset(&kp, 0, sizeof(kp));

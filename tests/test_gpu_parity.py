@@ -377,3 +377,21 @@ def test_mistral_layer_stack_pdl(M):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
     cols = np.arange(0, 6144, 97)[: 56]
     _sampled_cols_check(probs[0], ref[0], cols)
+
+
+@pytest.mark.parametrize("M,N,K,tn,sk", [(16, 512, 1024, 16, 2), (8, 256, 512, 16, 1), (130, 384, 768, 128, 3)])
+def test_ablation_smem_a_bit_identical(M, N, K, tn, sk):
+    """The shared-memory-A ablation (dequantized stage written back to SMEM + SS MMA)
+    computes exactly what the TMEM-A design computes (same MMAs in the same order)."""
+    ABL = 1 << 21
+    p = synth.make_problem(M + K, M=M, N=N, K=K, G=128)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    y0 = torch.empty((M, N), device=DEV, dtype=torch.float16)
+    y1 = torch.empty_like(y0)
+    h = torch.cuda.current_stream().cuda_stream
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y0.data_ptr(), h,
+                               quick.QUICK_FLAG_NO_STREAMK, tn, sk)
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y1.data_ptr(), h, ABL, tn, sk)
+    torch.cuda.synchronize()
+    assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+    check_tol(p, y1)
