@@ -57,6 +57,7 @@ constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per S
 constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
 constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
 constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memory (Cfg AM = 1)
+constexpr int kForcePair = 1 << 20;        // debug: CTA-pair (cta_group::2) plan for tiles 128/256
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -70,9 +71,16 @@ constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memor
 // AM (A-operand placement): 0 = the dequantized A stage in TMEM (tcgen05.st, TS MMA: the design);
 // 1 = ablation of the paper's Fig. 2 baseline on B200: the dequantized A stage written back to
 // shared memory (STS.128 in the UMMA SWIZZLE_128B K-major layout, conflict-free) and read by an SS
-// MMA (tiles 16 and 128, cluster split-K plans only)
+// MMA (tiles 16 and 128, cluster split-K plans only);
+// 2 = CTA pair (cta_group::2): two CTAs of a cluster on the two SMs of a TPC hold the weight
+// rows of two n-tiles (M = 256 across the pair, A in each CTA's TMEM) and load half of the BN
+// tokens of X each; the even CTA issues one MMA for both, so each SM reads half the X bytes
+// per weight row (the large-M regime is bound by the per-SM L2 -> SM input)
 template <int BN, bool SK, int AM = 0>
 struct Cfg {
+  static constexpr bool SMEM_A = AM == 1;
+  static constexpr bool PAIR = AM == 2;
+  static constexpr int XN = PAIR ? BN / 2 : BN;   // token rows of X this CTA loads
   // NPAR dequant groups of 4 warps.  NPAR = 4 (one CTA per SM, 16 dequant warps, the whole TMEM
   // for a 6-7 slot A ring) was measured 1.9x slower per SM than two 2-group CTAs per SM on the
   // 70B shapes at M <= 64 (one MMA warp per SM cannot keep up), so every tile uses 2 groups; the
@@ -87,17 +95,18 @@ struct Cfg {
   static constexpr int ASTAGES_FIT = (TMEM_BUDGET - NDBUF * (BN <= 32 ? 2 : 1) * BN) / kAColsPerStage;
   static constexpr int ASTAGES =
       NPAR == 4 ? (ASTAGES_FIT > 7 ? 7 : ASTAGES_FIT)
-                : (BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2));
-  static constexpr int DCOL = AM == 0 ? ASTAGES * kAColsPerStage : 0;   // A ring columns in TMEM
+                : (BN == 256 ? 4 : BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2));
+  static constexpr int DCOL = !SMEM_A ? ASTAGES * kAColsPerStage : 0;   // A ring columns in TMEM
   static constexpr int NACC = (BN <= 32 && DCOL + NDBUF * 2 * BN <= TMEM_BUDGET) ? 2 : 1;
   static constexpr int KL = BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
   static constexpr int STAGES = NPAR == 4 ? (BN <= 16 ? 8 : BN <= 32 ? 6 : 8)
-                                          : (BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 128 ? (AM ? 3 : 4) : 3);
-  static constexpr int X_BYTES = BN * KL * 2;       // [KL/64][BN][64] fp16, SW128 sub-tiles
-  static constexpr int X_SUB = BN * 128;            // one [BN][64] sub-tile (multiple of 1 KiB)
+                                          : (BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 128 ? (SMEM_A ? 3 : 4)
+                                                                                   : (PAIR ? 4 : 3));
+  static constexpr int X_BYTES = XN * KL * 2;       // [KL/64][XN][64] fp16, SW128 sub-tiles
+  static constexpr int X_SUB = XN * 128;            // one [XN][64] sub-tile (multiple of 1 KiB)
   static constexpr int W_BYTES = KL * 64;           // KL/32 chunks of 2 KiB
   static constexpr int M_BYTES = ((KL / 32 + 1) * kMetaBytes + 15) & ~15;  // worst case G = 32
   static constexpr int X_OFF = 0;
@@ -105,7 +114,7 @@ struct Cfg {
   static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
   static constexpr int A_BYTES = kTileRows * kKA * 2;   // AM = 1: one A stage in shared memory
   static constexpr int A_OFF = (M_OFF + STAGES * M_BYTES + 1023) & ~1023;
-  static constexpr int BAR_OFF = AM == 0 ? ((M_OFF + STAGES * M_BYTES + 7) & ~7) : (A_OFF + ASTAGES * A_BYTES);
+  static constexpr int BAR_OFF = !SMEM_A ? ((M_OFF + STAGES * M_BYTES + 7) & ~7) : (A_OFF + ASTAGES * A_BYTES);
   // barriers: full[STAGES], empty[STAGES], afull[ASTAGES], aempty[ASTAGES], dfull[2], dempty[2]
   // + xfull[STAGES]: the X tile has its own barrier so that dequantization (weights + metadata
   // only) can start before X is loadable (PDL: the weights of the first stages are fetched and
@@ -113,17 +122,18 @@ struct Cfg {
   static constexpr int NUM_BARS = 3 * STAGES + 2 * ASTAGES + 4;
   static constexpr int HOLD_OFF = BAR_OFF + NUM_BARS * 8;   // TMEM base, then stream-K flag
   static constexpr int USED = HOLD_OFF + 16;
-  static constexpr int TMEM_COLS = AM == 1 ? (NDBUF * NACC * BN <= 32 ? 32 : NDBUF * NACC * BN <= 64 ? 64
+  static constexpr int TMEM_COLS = SMEM_A ? (NDBUF * NACC * BN <= 32 ? 32 : NDBUF * NACC * BN <= 64 ? 64
                                                 : NDBUF * NACC * BN <= 128 ? 128 : 256)
                                    : ((NPAR == 2 && DCOL + NDBUF * NACC * BN <= 256) ? 256 : 512);
   // Cap co-resident CTAs per SM so that their TMEM allocations always fit (512 columns):
   // otherwise a cluster could wait on a CTA that spins in tcgen05.alloc.
-  static constexpr int MAX_CTAS_PER_SM = AM == 1 ? 1 : 512 / TMEM_COLS;
+  static constexpr int MAX_CTAS_PER_SM = SMEM_A ? 1 : 512 / TMEM_COLS;
   static constexpr int MIN_SMEM = (228 * 1024) / (MAX_CTAS_PER_SM + 1) + 1024;
   static constexpr int SMEM_BYTES = (USED + 1024 > MIN_SMEM ? USED + 1024 : MIN_SMEM);
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "tcgen05 M=128 needs N % 16 == 0, 16..256");
   static_assert(KL % kKA == 0 && APL <= 2, "load stage = one or two A stages");
   static_assert(!SK || BN <= 64, "stream-K is used for the small-M tiles");
+  static_assert(!PAIR || (!SK && BN >= 128), "CTA pairs: large-M cluster plans only");
   static_assert(ASTAGES >= NPAR && STAGES * APL >= NPAR, "ring indices advance by NPAR per group step");
   static_assert(DCOL + NDBUF * NACC * BN <= TMEM_COLS, "TMEM budget");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
@@ -155,12 +165,13 @@ struct Seg {
 
 // Enumerates this CTA's segments.  Cluster split-K: exactly one (blockIdx.y, blockIdx.z, the
 // split's A range).  Stream-K: the unit range of CTA blockIdx.x, cut at tile boundaries.
+// CTA pairs: blockIdx.x = 2 x split + member, n-tile 2 blockIdx.y + member.
 struct SegIter {
   int u, u1;
   int NA, m_tiles;
   bool sk, done;
   int t, mt, a_lo, a_hi;
-  __device__ __forceinline__ SegIter(const KParams& p, bool sk_) {
+  __device__ __forceinline__ SegIter(const KParams& p, bool sk_, bool pair = false) {
     sk = sk_;
     NA = p.NA;
     m_tiles = p.m_tiles;
@@ -170,11 +181,12 @@ struct SegIter {
       u = c * p.sk_q + min(c, p.sk_r);
       u1 = u + p.sk_q + (c < p.sk_r ? 1 : 0);
     } else {
-      const int S = gridDim.x;
-      t = blockIdx.y;
+      const int S = pair ? (int)gridDim.x >> 1 : (int)gridDim.x;
+      const int sp = pair ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
+      t = pair ? 2 * (int)blockIdx.y + ((int)blockIdx.x & 1) : (int)blockIdx.y;
       mt = blockIdx.z;
-      a_lo = (int)(((long long)blockIdx.x * NA) / S);
-      a_hi = (int)(((long long)(blockIdx.x + 1) * NA) / S);
+      a_lo = (int)(((long long)sp * NA) / S);
+      a_hi = (int)(((long long)(sp + 1) * NA) / S);
       u = u1 = 0;
     }
   }
@@ -277,10 +289,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   return d;
 }
 
-// tcgen05 instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M=128, N=BN
-template <int BN>
+// tcgen05 instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M=128 (256 for a
+// CTA pair), N=BN
+template <int BN, int MM = kTileRows>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
-  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
+  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
 }
 
 template <int BN, bool SK, bool GBIG, bool TRACE, int AM = 0>
@@ -297,6 +310,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   constexpr int APL = C::APL;
   constexpr int kAStages = C::ASTAGES;
   constexpr int kDCol = C::DCOL;
+  constexpr bool PAIR = C::PAIR;
+  // afull arrivals: one per dequant warp for CTA pairs (remote arrivals are expensive); one per
+  // thread otherwise (per-warp arrivals measured 0-3 % slower at small M on one CTA)
+  constexpr bool kWarpArrive = PAIR;
   if (p.flags & kDebugExitTop) return;
   extern __shared__ uint8_t smem_raw[];
   // 1 KiB-aligned base, computed in the 32-bit shared window (cheap to rematerialise)
@@ -306,7 +323,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int K = p.K, G = p.G, M = p.M;
-  const int S = SK ? 1 : (int)gridDim.x;   // cluster split-K factor
+  const int S = SK ? 1 : (PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x);   // cluster split-K factor
+  // CTA pair: cluster rank 2 x split + member; the even member (leader) issues the MMAs
+  const uint32_t crank = PAIR ? ptx::cluster_ctarank() : 0u;
+  const uint32_t member = crank & 1u;
+  const uint32_t lead_rank = crank & ~1u;
   const int C32 = K / 32;
   const int NG = K / G;
   const bool out_fp32 = (p.flags & QUICK_FLAG_OUT_F32) != 0;
@@ -338,7 +359,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       ptx::mbar_init(bar_empty + 8 * s, 4 * 32 * APL + 1);
     }
     for (int a = 0; a < kAStages; ++a) {
-      ptx::mbar_init(bar_afull + 8 * a, 4 * 32);      // every thread of one parity group
+      // every thread of one parity group (CTA pair: one arrival per warp of both members)
+      ptx::mbar_init(bar_afull + 8 * a, kWarpArrive ? (PAIR ? 8 : 4) : 4 * 32);
       ptx::mbar_init(bar_aempty + 8 * a, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -353,19 +375,31 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     __syncwarp();
     ptx::named_bar_arrive(2, kThreads);
   } else {
-    if (warp == kMmaWarp) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), C::TMEM_COLS);
+    if (warp == kMmaWarp) {
+      if constexpr (PAIR)
+        ptx::tmem_alloc2(ptx::smem_u32(tmem_holder), C::TMEM_COLS);
+      else
+        ptx::tmem_alloc(ptx::smem_u32(tmem_holder), C::TMEM_COLS);
+    }
     ptx::tc_fence_before();
     ptx::named_bar_sync(2, kThreads);
     ptx::tc_fence_after();
     tmem = *tmem_holder;
   }
+  // CTA pair: the peer's barriers must be initialised before any remote arrival or TMA
+  // completion targets them
+  if constexpr (PAIR) ptx::cluster_sync();
   if (p.flags & kDebugExitPrologue) {
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == kMmaWarp) {
       ptx::tc_fence_after();
-      ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+      if constexpr (PAIR)
+        ptx::tmem_dealloc2(tmem, C::TMEM_COLS);
+      else
+        ptx::tmem_dealloc(tmem, C::TMEM_COLS);
     }
+    if constexpr (PAIR) ptx::cluster_sync();
     return;
   }
   // debug tracing (TRACE instantiation only, tools/trace_gemm.py): clock64 stamps per stage
@@ -395,11 +429,23 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     // stages never straddle segments (the last one of a segment may be short).
     const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
-    SegIter it(p, SK);
+    SegIter it(p, SK, C::PAIR);
     Seg sg;
     int slot = 0, lf = 0;
     uint32_t ph = 0;
     int pre = -1;   // PDL: weight copies of the first `pre` load stages go before the X wait
+    // X tile of load stage `j` into slot `xs`.  CTA pair: each member loads its half of the
+    // tokens; both halves complete on the leader's xfull barrier, which expects both
+    auto load_x = [&](int xs, int m0, int kc) {
+      if constexpr (PAIR) {
+        if (member == 0) ptx::mbar_arrive_expect_tx(bar_xfull + 8 * xs, 2 * C::X_BYTES);
+        ptx::tma_load_3d_pair(sbase + C::X_OFF + xs * C::X_BYTES, &tmap_x, 0, m0 + (int)member * C::XN, kc,
+                              ptx::mapa(bar_xfull + 8 * xs, lead_rank), pol_x);
+      } else {
+        ptx::mbar_arrive_expect_tx(bar_xfull + 8 * xs, C::X_BYTES);
+        ptx::tma_load_3d_hint(sbase + C::X_OFF + xs * C::X_BYTES, &tmap_x, 0, m0, kc, bar_xfull + 8 * xs, pol_x);
+      }
+    };
     while (it.next(sg)) {
       const uint8_t* wbase = p.packed + (size_t)sg.t * C32 * kChunkBytes;
       const uint8_t* mbase = p.packed + (size_t)K * p.N / 2 + (size_t)sg.t * NG * kMetaBytes;
@@ -428,16 +474,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           ptx::bulk_load_hint(sbase + C::M_OFF + slot * C::M_BYTES,
                               mbase + (size_t)g0 * kMetaBytes, meta_bytes, full, pol_w);
           if (lf >= pre && !(pre == 0 && lf == 0)) {
-            ptx::mbar_arrive_expect_tx(bar_xfull + 8 * slot, C::X_BYTES);
-            ptx::tma_load_3d_hint(sbase + C::X_OFF + slot * C::X_BYTES, &tmap_x, 0, m0, kl0 / 64,
-                                  bar_xfull + 8 * slot, pol_x);
+            load_x(slot, m0, kl0 / 64);
           } else if (lf == (pre > 0 ? pre - 1 : 0)) {
             if (pdl) ptx::griddep_wait();
-            for (int j = 0; j <= lf; ++j) {   // X of the stages issued so far (all in this segment)
-              ptx::mbar_arrive_expect_tx(bar_xfull + 8 * j, C::X_BYTES);
-              ptx::tma_load_3d_hint(sbase + C::X_OFF + j * C::X_BYTES, &tmap_x, 0, m0,
-                                    (sg.a_lo + j * APL) * kKA / 64, bar_xfull + 8 * j, pol_x);
-            }
+            for (int j = 0; j <= lf; ++j)   // X of the stages issued so far (all in this segment)
+              load_x(j, m0, (sg.a_lo + j * APL) * kKA / 64);
           }
         }
         __syncwarp();
@@ -453,24 +494,42 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     // ------------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; one elected lane issues the MMAs and the commits (a commit tracks
     // the async tcgen05 ops of the thread that issues it, so the same lane does both).
-    constexpr uint32_t idesc = instr_desc<BN>();
+    constexpr uint32_t idesc = instr_desc<BN, PAIR ? 2 * kTileRows : kTileRows>();
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
     // AM = 1: the A stage is an SW128 K-major tile in shared memory (two 64-k sub-tiles of 16 KiB)
     const uint64_t adesc0 = sw128_desc(sbase + (uint32_t)C::A_OFF);
     // one K=16 MMA of A stage `a_slot`; `a_col` is its TMEM column (AM = 0)
     auto mma_k = [&](uint32_t d, uint32_t a_col, int a_slot, int kk, uint64_t bdesc, uint32_t acc) {
-      if constexpr (AM == 0) {
+      if constexpr (PAIR) {
+        ptx::mma2_f16_ts(d, a_col + kk * 8, bdesc, idesc, acc);
+      } else if constexpr (!C::SMEM_A) {
         ptx::mma_f16_ts(d, a_col + kk * 8, bdesc, idesc, acc);
       } else {
         ptx::mma_f16_ss(d, adesc0 + (uint64_t)((a_slot * C::A_BYTES + (kk >> 2) * (kTileRows * 128)) >> 4) +
                                (uint64_t)((kk & 3) * 2), bdesc, idesc, acc);
       }
     };
-    SegIter it(p, SK);
+    // completion of the MMAs issued so far -> barrier (both members' copies for a pair)
+    const uint16_t cmask = (uint16_t)(3u << lead_rank);
+    auto commit = [&](uint32_t bar) {
+      if constexpr (PAIR)
+        ptx::mma2_commit(bar, cmask);
+      else
+        ptx::mma_commit(bar);
+    };
+    SegIter it(p, SK, C::PAIR);
     Seg sg;
     int slot = 0, as = 0, si = 0, ia = 0, lf_mma = 0;
     uint32_t aph = 0, xph = 0;
-    while (it.next(sg)) {
+    // CTA pair: the odd member issues nothing; it only counts the stages for the drain below
+    // (the leader's commits arrive on its barriers too)
+    if (PAIR && member != 0) {
+      while (it.next(sg)) {
+        ia += sg.a_hi - sg.a_lo;
+        lf_mma += (sg.a_hi - sg.a_lo + APL - 1) / APL;
+      }
+    }
+    while ((!PAIR || member == 0) && it.next(sg)) {
       const int db = SK ? (si & 1) : 0;
       // stream-K: the accumulator of segment si - 2 must have been read out
       if (SK && si >= 2) ptx::mbar_wait(bar_dempty + 8 * db, (uint32_t)(((si >> 1) + 1) & 1));
@@ -500,8 +559,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
                 mma_k(d_col + (uint32_t)((kk % C::NACC) * BN), a_col, as, kk,
                       dstage + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), 1u);
             }
-            ptx::mma_commit(bar_aempty + 8 * as);
-            if (APL == 1) ptx::mma_commit(bar_empty + 8 * slot);
+            commit(bar_aempty + 8 * as);
+            if (APL == 1) commit(bar_empty + 8 * slot);
           }
           __syncwarp();
           ptx::mbar_wait(bar_afull + 8 * as1, aph1);
@@ -517,9 +576,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
                 mma_k(d_col + (uint32_t)((kk % C::NACC) * BN), a_col, as1, kk,
                       d1 + (uint64_t)((kk >> 2) * (C::X_SUB >> 4) + (kk & 3) * 2), 1u);
             }
-            ptx::mma_commit(bar_aempty + 8 * as1);
-            ptx::mma_commit(bar_empty + 8 * slot1);
-            if (a + 1 == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
+            commit(bar_aempty + 8 * as1);
+            commit(bar_empty + 8 * slot1);
+            if (a + 1 == sg.a_hi - 1) commit(bar_dfull + 8 * db);
           }
           __syncwarp();
           ++a;
@@ -545,9 +604,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         const bool last_of_load = (sub == APL - 1) || (a == sg.a_hi - 1);
         if (ptx::elect_one()) {
           if (dbg_skip) {
-            ptx::mma_commit(bar_aempty + 8 * as);
-            if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);
-            if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);
+            commit(bar_aempty + 8 * as);
+            if (last_of_load) commit(bar_empty + 8 * slot);
+            if (a == sg.a_hi - 1) commit(bar_dfull + 8 * db);
           } else {
           const uint32_t a_col = tmem + as * kAColsPerStage;
           // descriptor start address in 16-B units: X slot, 64-k sub-tile, then 32 B per K=16
@@ -569,9 +628,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
                       (first && kk < C::NACC) ? 0u : 1u);
             }
           }
-          ptx::mma_commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
-          if (last_of_load) ptx::mma_commit(bar_empty + 8 * slot);   // X of this load stage used
-          if (a == sg.a_hi - 1) ptx::mma_commit(bar_dfull + 8 * db);  // segment accumulated
+          commit(bar_aempty + 8 * as);    // A stage free once these MMAs complete
+          if (last_of_load) commit(bar_empty + 8 * slot);   // X of this load stage used
+          if (a == sg.a_hi - 1) commit(bar_dfull + 8 * db);  // segment accumulated
           }
         }
         __syncwarp();
@@ -647,12 +706,29 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       return c;
     };
     const bool tw = TRACE && (warp == 0 && lane == 0);
+    // A stage written: CTA pair members both arrive on the leader's afull (its MMA reads both
+    // halves of A from the two TMEMs), one arrival per warp after a warp sync (128 remote
+    // per-thread arrivals per stage were measured ~750 cycles slower than local ones)
+    const uint32_t afull_lead = PAIR ? ptx::mapa(bar_afull, lead_rank) : 0u;
+    auto arrive_afull = [&](int as_) {
+      if constexpr (kWarpArrive) {
+        __syncwarp();
+        if (lane == 0) {
+          if (member != 0)
+            ptx::mbar_arrive_remote(afull_lead + 8u * (uint32_t)as_);
+          else
+            ptx::mbar_arrive(bar_afull + 8 * as_);
+        }
+      } else {
+        ptx::mbar_arrive(bar_afull + 8 * as_);
+      }
+    };
     // epilogue: the accumulator columns are split over the groups in chunks of >= 8
     constexpr int kColsPerWarp = BN / NPAR >= 8 ? BN / NPAR : 8;
     const int j0 = par * kColsPerWarp;   // this warp's share of the accumulator columns
     const int jend = min(j0 + kColsPerWarp, BN);
     uint32_t a_regs[32];
-    SegIter it(p, SK);
+    SegIter it(p, SK, C::PAIR);
     Seg sg;
     int ia = 0, si = 0, lbase = 0;       // flat A-stage index, segment index, first load stage
     while (it.next(sg)) {
@@ -705,7 +781,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           ptx::mbar_arrive_cnt(bar_empty + 8 * slot, cnt);
           if (dbg_nocompute) {
             ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
-            ptx::mbar_arrive(bar_afull + 8 * as);
+            arrive_afull(as);
           } else {
             dequant_word(w[0].x, cst, a_regs + 0);
             dequant_word(w[0].y, cst, a_regs + 4);
@@ -775,7 +851,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
               ptx::tmem_wait_st();
               ptx::tc_fence_before();
             }
-            ptx::mbar_arrive(bar_afull + 8 * as);
+            arrive_afull(as);
             if (tw) stamp(4, iw);
           }
           slot += NPAR / APL;
@@ -929,14 +1005,15 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     ptx::cluster_sync();
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[6] = clock64();
     const int m0 = blockIdx.z * BN;
-    const uint32_t my = ptx::cluster_ctarank();
+    const uint32_t my = PAIR ? (crank >> 1) : ptx::cluster_ctarank();   // split index
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
     const int eb = (int)(((int)my * E4) / S) * 4;
     const int ee = (int)((((int)my + 1) * E4) / S) * 4;
     const int e_lim = min(ee, max(0, (M - m0)) * kTileRows);   // skip padded tokens
     uint32_t peer[kMaxSplit];
 #pragma unroll
-    for (int q = 0; q < kMaxSplit; ++q) peer[q] = ptx::mapa(sbase, (uint32_t)(q < S ? q : 0));
+    for (int q = 0; q < kMaxSplit; ++q)   // (pair: the same member of each split's pair)
+      peer[q] = ptx::mapa(sbase, PAIR ? (uint32_t)(2 * (q < S ? q : 0)) + member : (uint32_t)(q < S ? q : 0));
     for (int e = eb + (int)threadIdx.x * 4; e < e_lim; e += kThreads * 4) {
       float4 v[kMaxSplit];
 #pragma unroll
@@ -953,7 +1030,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         }
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
-      const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)blockIdx.y * kTileRows + rr;
+      const int tt = PAIR ? 2 * (int)blockIdx.y + (int)member : (int)blockIdx.y;
+      const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * kTileRows + rr;
       if (out_fp32) {
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
       } else {
@@ -988,7 +1066,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   if (TRACE && tr != nullptr && threadIdx.x == 0) {
     tr[2] = clock64();
     int na_total = 0;
-    SegIter it(p, SK);
+    SegIter it(p, SK, C::PAIR);
     Seg sg;
     while (it.next(sg)) na_total += sg.a_hi - sg.a_lo;
     tr[3] = (unsigned long long)na_total;
@@ -996,11 +1074,22 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tr[4] = smid;
   }
-  if (warp == kMmaWarp) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  if constexpr (PAIR) {
+    // both members' MMAs are complete (each waited its dfull); release the pair allocation
+    // together
+    if (S == 1) ptx::cluster_arrive();
+    ptx::cluster_wait();
+    if (warp == kMmaWarp) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc2(tmem, C::TMEM_COLS);
+    }
+  } else {
+    if (warp == kMmaWarp) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+    if (!SK && S > 1) ptx::cluster_wait();   // (arrived after the split-K reduce)
   }
-  if (!SK && S > 1) ptx::cluster_wait();   // (arrived after the split-K reduce)
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1242,6 +1331,53 @@ int max_resident(int bn, bool sk, int S) {
   return n;
 }
 
+// CTA pairs (tiles 128 / 256, no stream-K): the kernel, and how many clusters of 2 S CTAs
+// (S splits of a pair) can be resident at once
+template <int BN>
+void* pair_kernel(bool gbig) {
+  return gbig ? reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, false, true, false, 2>)
+              : reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, false, false, false, 2>);
+}
+int max_resident_pair(int bn, int S) {
+  static std::mutex mu;
+  static int cache[kMaxDev][2][quick::kMaxSplit + 1] = {};
+  const int dev = current_device(), ti = bn == 256 ? 1 : 0;
+  if (S < 1 || 2 * S > quick::kMaxSplit) return 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache[dev][ti][S]) return cache[dev][ti][S];
+  }
+  const int smem = bn == 256 ? quick::Cfg<256, false, 2>::SMEM_BYTES : quick::Cfg<128, false, 2>::SMEM_BYTES;
+  const int threads = quick::Cfg<128, false, 2>::THREADS;
+  const int per_sm_tmem = bn == 256 ? quick::Cfg<256, false, 2>::MAX_CTAS_PER_SM
+                                    : quick::Cfg<128, false, 2>::MAX_CTAS_PER_SM;
+  int n = 0;
+  void* k = bn == 256 ? pair_kernel<256>(true) : pair_kernel<128>(true);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)(2 * S), 1, 1);
+    cfg.blockDim = dim3((unsigned)threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = (unsigned)(2 * S);
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) n = 0;
+    // the query assumes one CTA per SM (see max_resident)
+    const int per_sm = std::min(per_sm_tmem, (228 * 1024) / (smem + 1024));
+    if (per_sm >= 2) n = std::max(n, (per_sm * sm_count() * 9) / (10 * 2 * S));
+  }
+  cudaGetLastError();
+  if (n <= 0) n = std::max(1, sm_count() / (4 * S));
+  std::lock_guard<std::mutex> lock(mu);
+  cache[dev][ti][S] = n;
+  return n;
+}
+
 // ---------------------------------------------------------------------------------------
 // Stream-K workspace: per (device, stream), allocated on the first call outside graph
 // capture (partial tiles [P][2][BN][128] fp32 + one arrival counter per tile, zeroed once and
@@ -1305,12 +1441,13 @@ struct Plan {
   int tile_n, split, ctas;
   bool sk;
   int P;   // stream-K CTAs
+  bool pair = false;   // CTA pairs (cta_group::2), tiles 128 / 256 (split = splits per pair)
 };
 
 constexpr int kMaxAccumK = 8192;
 
-// tile 256 (1 CTA/SM, 2-stage ring) measured slower than tile 128 at every M >= 128 on B200
-// (tools/tune_plan.py), so the automatic plan tiles large M by 128 tokens
+// the smallest tile covering M (at most 128; M > 64 goes through the cost model below, which
+// also considers 256-token tiles and CTA pairs)
 int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128; }
 
 // Launch plan (tuned with tools/tune_plan.py on B200):
@@ -1318,10 +1455,12 @@ int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
 //    per m-tile; M > 128 tiles the tokens by 128);
 //  - tiles <= 64 (the HBM-bound regime): stream-K over (tile, 128-k stage) units with one wave
 //    of 2 CTAs per SM, each CTA a contiguous range of >= 4 units;
-//  - otherwise split-K over a cluster: the largest S <= 8 such that all tiles x S CTAs are
+//  - M > 64 (tensor-bound): the fitted cost model over tile {128, 256}, split S and CTA pairs;
+//  - otherwise split-K over a cluster: the largest S <= 6 such that all tiles x S CTAs are
 //    resident in one wave (clusters are GPC-placed, so residency is queried) and every CTA
-//    keeps >= 2 A stages; then S >= ceil(K / 8192) for accuracy (a TMEM accumulator sums at
-//    most 8192 of K, R15).
+//    keeps >= 2 A stages;
+//  - always S >= ceil(K / 8192) for accuracy (a TMEM accumulator sums at most 8192 of K,
+//    DESIGN.md R15).
 Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bool allow_sk) {
   (void)G;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
@@ -1343,30 +1482,38 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
       return Plan{tn, 1, (int)P, true, (int)P};
   }
   const int s_min = (K + kMaxAccumK - 1) / kMaxAccumK;
-  if (force_tile == 0 && force_split == 0 && M > 128) {
-    // Large M (tensor-bound): cost model over tile in {128, 256} tokens and split S, in cycles
-    // per SM: waves x (A stages per CTA x stage time + fixed per-CTA cost).  Measured stage
-    // times on B200 (tools/trace_gemm.py): 128 x 128 tokens ~700 cycles (8 MMAs of 512 + issue
-    // gaps), 128 x 256 tokens ~1280 (MMA pipe ~80 % busy); ~7000 cycles of prologue/epilogue
-    // per CTA; a DSMEM split-K reduce costs two cluster barriers (~2500) + the partial tile
-    // through shared memory (~128 B/clk) + its remote (S-1)/S share through DSMEM (~20 B/clk,
-    // measured: a 128 KiB partial at S = 4 takes ~9000 cycles).  Waves count resident clusters.
+  if (force_tile == 0 && force_split == 0 && M > 64) {
+    // Tensor-bound regime: cost model over tile {128, 256} tokens x split S x CTA pairs
+    // (cta_group::2), fitted on B200 to 280 forced-plan timings (tools/sweep.py modes
+    // t<tile>s<S>[p], 5 shapes x M = 128..1024, PDL chains; rms error 10 %):
+    //   time = waves x (A stages per CTA x st + fixed + [S > 1] 1.93 + 0.355 (cluster - 1)
+    //          + [cluster == 8] 1.21)   (microseconds)
+    // with waves = ceil(clusters / resident clusters) (queried: GPC placement).  Per-stage
+    // costs: tile 128 0.486 us (pair 0.648 for twice the rows per cluster), tile 256 0.752
+    // (pair 0.665): the pair halves each SM's X traffic, which bounds the large tiles.
+    static const double st[2][2] = {{0.486, 0.648}, {0.752, 0.665}};
+    static const double fixed[2][2] = {{3.226, 2.733}, {4.748, 4.455}};
+    const int n_tiles = N / quick::kTileRows;
     double best = 1e300;
-    Plan bp{128, 1, 0, false, 0};
+    Plan bp{128, std::max(1, s_min), 0, false, 0};
     for (int tc : {128, 256}) {
-      const int tl = (N / quick::kTileRows) * ((M + tc - 1) / tc);
-      const double stage = tc == 256 ? 1280.0 : 700.0;
-      for (int s2 = 1; s2 <= quick::kMaxSplit; ++s2) {
-        if (s2 < s_min) continue;
-        if (s2 > 1 && s2 > NA / 2) break;
-        const int res = max_resident(tc, false, s2);
-        const long long waves = ((long long)tl + res - 1) / res;
-        const double part = (double)tc * quick::kTileRows * 4.0;   // fp32 partial tile bytes
-        const double red = s2 > 1 ? 2500.0 + part / 128.0 + part * (s2 - 1) / s2 / 20.0 : 0.0;
-        const double t = (double)waves * (((NA + s2 - 1) / s2) * stage + 7000.0 + red);
-        if (t < best) {
-          best = t;
-          bp = Plan{tc, s2, tl * s2, false, 0};
+      if (tc == 256 && M <= 128) continue;
+      const int mt = (M + tc - 1) / tc;
+      for (int pr = 0; pr < 2; ++pr) {
+        if (pr && n_tiles % 2 != 0) continue;
+        for (int s2 = 1; s2 <= (pr ? quick::kMaxSplit / 2 : quick::kMaxSplit); ++s2) {
+          if (s2 < s_min) continue;
+          if (s2 > 1 && s2 > NA / 2) break;
+          const long long units = (long long)(n_tiles / (pr ? 2 : 1)) * mt;
+          const int res = pr ? max_resident_pair(tc, s2) : max_resident(tc, false, s2);
+          const long long waves = (units + res - 1) / res;
+          const int csz = s2 * (pr ? 2 : 1);
+          const double t = (double)waves * (((NA + s2 - 1) / s2) * st[tc == 256][pr] + fixed[tc == 256][pr] +
+                                            (s2 > 1 ? 1.933 : 0.0) + 0.355 * (csz - 1) + (csz == 8 ? 1.209 : 0.0));
+          if (t < best) {
+            best = t;
+            bp = Plan{tc, s2, n_tiles * mt * s2, false, 0, pr != 0};
+          }
         }
       }
     }
@@ -1396,7 +1543,7 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
 
 template <int BN, bool SK>
 quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int P,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, bool pair = false) {
   using C = quick::Cfg<BN, SK>;
   cudaError_t e = configure_kernel(BN, SK);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -1430,6 +1577,35 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   // group-size specialisation: a power of two >= 128 (the group index is a shift and an A
   // stage never straddles groups); any other G takes the per-32-k general path
   const bool gbig = kp.G >= quick::kKA && (kp.G & (kp.G - 1)) == 0;
+  if constexpr (!SK && BN >= 128) {
+    if (pair) {   // CTA pairs (cta_group::2): grid (2 S, n_tiles / 2, m_tiles), clusters of 2 S
+      using CP = quick::Cfg<BN, false, 2>;
+      auto* kq = g_trace != nullptr ? (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, true, 2>
+                                            : quick::quick_w4a16_tc_kernel<BN, false, false, true, 2>)
+                                    : (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, false, 2>
+                                            : quick::quick_w4a16_tc_kernel<BN, false, false, false, 2>);
+      e = cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::SMEM_BYTES);
+      if (e != cudaSuccess) return cuda_fail(e);
+      cfg.gridDim = dim3((unsigned)(2 * S), (unsigned)(kp.n_tiles / 2), (unsigned)kp.m_tiles);
+      cfg.dynamicSmemBytes = CP::SMEM_BYTES;
+      cfg.blockDim = dim3((unsigned)CP::THREADS, 1, 1);
+      na = 0;
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = (unsigned)(2 * S);
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+      if (kp.flags & QUICK_FLAG_PDL) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+      }
+      cfg.numAttrs = na;
+      e = cudaLaunchKernelEx(&cfg, kq, tmap, kp);
+      if (e != cudaSuccess) return cuda_fail(e);
+      return QUICK_OK;
+    }
+  }
   if constexpr (!SK && (BN == 16 || BN == 128)) {
     if (kp.flags & quick::kAblationSmemA) {   // the shared-memory-A ablation
       using CA = quick::Cfg<BN, false, 1>;
@@ -1472,6 +1648,7 @@ void quick_debug_set_trace(void* device_buffer) {
 // Debug only: resident CTAs (S == 1) or clusters (S > 1) of the (tile, stream-K) kernel, and
 // its dynamic shared memory bytes.
 int quick_debug_resident(int bn, int sk, int S, int* smem_bytes, int* regs) {
+  if (sk == 2) return (bn == 128 || bn == 256) ? max_resident_pair(bn, S) : -1;   // CTA pairs
   if (tile_index(bn) < 0 || S < 1 || S > quick::kMaxSplit || (sk && !sk_capable(bn))) return -1;
   if (smem_bytes) *smem_bytes = smem_for(bn, sk != 0);
   if (regs) {
@@ -1479,6 +1656,12 @@ int quick_debug_resident(int bn, int sk, int S, int* smem_bytes, int* regs) {
     *regs = cudaFuncGetAttributes(&fa, kernel_for(bn, sk != 0)) == cudaSuccess ? fa.numRegs : -1;
   }
   return max_resident(bn, sk != 0, S);
+}
+
+// Debug only: 1 when the automatic plan of this shape uses CTA pairs (cta_group::2)
+int quick_debug_plan_pair(int M, int N, int K, int G) {
+  if (check_gemm_shape(M, N, K, G) != QUICK_OK) return -1;
+  return choose_plan(M > 0 ? M : 1, N, K, G, 0, 0, true).pair ? 1 : 0;
 }
 
 quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* split_k,
@@ -1503,7 +1686,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
                     quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly | quick::kAblationSmemA;
+                    quick::kDebugPdlEarly | quick::kAblationSmemA | quick::kForcePair;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1514,6 +1697,9 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   Plan plan = choose_plan(M, N, K, G, tile_n, split_k,
                           (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0);
   if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
+  if ((flags & quick::kForcePair) && !plan.sk && plan.tile_n >= 128 && (N / quick::kTileRows) % 2 == 0 &&
+      2 * plan.split <= quick::kMaxSplit)
+    plan.pair = true;
   quick::KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.n_tiles = N / quick::kTileRows;
@@ -1539,7 +1725,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int kl = kl_for(tn, plan.sk);
   cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
   cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
-  cuuint32_t box[3] = {64, (cuuint32_t)tn, (cuuint32_t)(kl / 64)};
+  cuuint32_t box[3] = {64, (cuuint32_t)(plan.pair ? tn / 2 : tn), (cuuint32_t)(kl / 64)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(X), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1575,8 +1761,8 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
     case 16: return launch_bn<16, false>(tmap, kp, s, 0, strm);
     case 32: return launch_bn<32, false>(tmap, kp, s, 0, strm);
     case 64: return launch_bn<64, false>(tmap, kp, s, 0, strm);
-    case 128: return launch_bn<128, false>(tmap, kp, s, 0, strm);
-    default: return launch_bn<256, false>(tmap, kp, s, 0, strm);
+    case 128: return launch_bn<128, false>(tmap, kp, s, 0, strm, plan.pair);
+    default: return launch_bn<256, false>(tmap, kp, s, 0, strm, plan.pair);
   }
 }
 

@@ -111,7 +111,8 @@ def quick_gemm_plan(M: int, N: int, K: int, group_size: int):
     tn, sk, nc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     _check("quick_gemm_plan", _lib.quick_gemm_plan(M, N, K, group_size, ctypes.byref(tn), ctypes.byref(sk),
                                                    ctypes.byref(nc)))
-    return {"tile_n": tn.value, "split_k": sk.value, "num_ctas": nc.value}
+    pair = _lib.quick_debug_plan_pair(M, N, K, group_size) == 1   # CTA pairs (cta_group::2)
+    return {"tile_n": tn.value, "split_k": sk.value, "num_ctas": nc.value, "pair": pair}
 
 
 # ----------------------------------------------------------------------------- device side

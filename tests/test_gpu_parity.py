@@ -290,20 +290,25 @@ def test_pdl_chain_matches_ordinary_launches(M, N, K):
     check_tol(p1, y1)
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 28672, 8192), (512, 5120, 13824)])
-def test_pdl_wide_tile_multiwave_stress(M, N, K):
-    """The 256-token tile on multi-wave grids under back-to-back PDL launches (the configuration
-    whose deeper weight prefetch failed intermittently): 24 launches, each
-    bit-identical to an ordinary launch."""
+@pytest.mark.parametrize("M,N,K,S,pair", [(256, 28672, 8192, 1, False), (512, 5120, 13824, 3, False),
+                                          (256, 28672, 8192, 1, True), (1024, 13824, 5120, 1, True),
+                                          (512, 5120, 13824, 2, True)])
+def test_pdl_wide_tile_multiwave_stress(M, N, K, S, pair):
+    """The 256-token tile (one CTA, or a CTA pair) on multi-wave grids under back-to-back PDL
+    launches (the configuration whose deeper weight prefetch failed intermittently, DESIGN.md
+    §5.4): 24 launches, each bit-identical to an ordinary launch."""
     G = 128
     p = synth.make_problem(M ^ K, M=M, N=N, K=K, G=G)
-    assert quick.quick_gemm_plan(M, N, K, G)["tile_n"] == 256
     x, w = to_dev_f16(p.x), pack_dev(p)
-    ref = quick.quick_w4a16_gemm(x, w, N, K, G)
+    h = torch.cuda.current_stream().cuda_stream
+    fl = PAIR if pair else 0
+    ref = torch.empty((M, N), device=DEV, dtype=torch.float16)
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), w.data_ptr(), M, N, K, G, ref.data_ptr(), h, fl, 256, S)
     torch.cuda.synchronize()
     outs = [torch.empty_like(ref) for _ in range(3)]
     for i in range(24):
-        quick.quick_w4a16_gemm(x, w, N, K, G, out=outs[i % 3], pdl=True)
+        quick.quick_w4a16_gemm_raw(x.data_ptr(), w.data_ptr(), M, N, K, G, outs[i % 3].data_ptr(), h,
+                                   fl | quick.QUICK_FLAG_PDL, 256, S)
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
@@ -395,3 +400,55 @@ def test_ablation_smem_a_bit_identical(M, N, K, tn, sk):
     torch.cuda.synchronize()
     assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
     check_tol(p, y1)
+
+
+# ------------------------------------------------------------------------------- CTA pairs
+PAIR = 1 << 20   # internal flag: force the CTA-pair (cta_group::2) variant of a tile-128/256 plan
+
+
+@pytest.mark.parametrize("M,N,K,tn,sk", [(256, 512, 512, 256, 1), (200, 256, 1024, 128, 1), (130, 768, 1280, 128, 3),
+                                         (300, 512, 2048, 256, 2), (97, 1024, 640, 128, 4), (256, 256, 384, 256, 3)])
+def test_pair_bit_identical_and_oracle(M, N, K, tn, sk):
+    """CTA pairs (M = 256 MMAs over two SMs, X split by tokens between the pair):
+    the same MMAs in the same K order as one CTA per n-tile, so bit-identical to the ordinary plan
+    of that tile/split, and within tolerance of the oracle.  Ragged M, ragged K (K % 128 = 64),
+    odd A-stage splits and one-cluster-of-8 (S = 4) cases."""
+    p = synth.make_problem(M + K + 7, M=M, N=N, K=K, G=128)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    y0 = torch.full((M, N), float("nan"), device=DEV, dtype=torch.float16)
+    y1 = torch.full((M, N), float("nan"), device=DEV, dtype=torch.float16)
+    h = torch.cuda.current_stream().cuda_stream
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y0.data_ptr(), h, 0, tn, sk)
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y1.data_ptr(), h, PAIR, tn, sk)
+    torch.cuda.synchronize()
+    assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+    check_tol(p, y1)
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 28672, 8192), (256, 13824, 5120), (512, 4096, 4096), (128, 8192, 28672)])
+def test_pair_auto_plan_full_size_pdl(M, N, K):
+    """The automatic plan picks CTA pairs for these large-M shapes; launched as a PDL chain in a CUDA
+    graph (the bench's mode) the result is bit-identical to ordinary launches of the same plan, and
+    sampled columns are within tolerance of the oracle."""
+    pl = quick.quick_gemm_plan(M, N, K, 128)
+    assert pl["pair"], pl
+    p = synth.make_problem(M * 3 + N, M=M, N=N, K=K, G=128)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    y0 = torch.empty((M, N), device=DEV, dtype=torch.float16)
+    quick.quick_w4a16_gemm(x, blob, N, K, 128, out=y0)
+    ys = [torch.empty_like(y0) for _ in range(3)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        quick.quick_w4a16_gemm(x, blob, N, K, 128, out=ys[0], pdl=True)   # eager warm-up
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for y in ys:
+                quick.quick_w4a16_gemm(x, blob, N, K, 128, out=y, pdl=True)
+        g.replay()
+    torch.cuda.synchronize()
+    for y in ys:
+        assert torch.equal(y0.view(torch.int16), y.view(torch.int16))
+    rng = np.random.default_rng(N)
+    cols = np.unique(np.concatenate([np.arange(8), np.arange(N - 8, N), rng.choice(N, 112, replace=False)]))
+    cols = cols[:len(cols) // 8 * 8]
+    _sampled_cols_check(p, y0, cols)

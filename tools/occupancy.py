@@ -18,3 +18,8 @@ for bn in (16, 32, 64, 128, 256):
         sm, rg = ctypes.c_int(), ctypes.c_int()
         res = [f(bn, sk, S, ctypes.byref(sm), ctypes.byref(rg)) for S in (1, 2, 4, 8)]
         print(f"tile {bn:3d} sk {sk}: smem {sm.value} B regs {rg.value}  resident S=1,2,4,8: {res}")
+res = {}
+for bn in (128, 256):
+    res[f"t{bn}"] = [f(bn, 0, S, None, None) for S in range(1, 9)]
+    res[f"t{bn}p"] = [f(bn, 2, S, None, None) for S in range(1, 5)]
+print("resident (S = 1..):", res)

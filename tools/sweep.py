@@ -71,10 +71,13 @@ for (N, K) in SHAPES[which]:
         F = 2 * M * N * K
         rec = {"N": N, "K": K, "M": M, "plan": quick.quick_gemm_plan(M, N, K, G)}
         for mode in modes:
-            # "auto" / "pdl" / "nosk", or a forced plan "t<tile>s<split>" (e.g. t256s2)
+            # "auto" / "pdl" / "nosk", or a forced plan "t<tile>s<split>[p]" (e.g. t256s2, t256s2p)
             fl, tn, sk = FLAGS.get(mode, 0), 0, 0
-            if mode.startswith("t"):
-                tn, sk = (int(v) for v in mode[1:].split("s"))
+            if mode.startswith("t"):   # "t<tile>s<split>[p]": p = CTA pair (cta_group::2)
+                fl = quick.QUICK_FLAG_PDL   # forced plans are timed with PDL, like the bench
+                if mode.endswith("p"):
+                    fl |= 1 << 20
+                tn, sk = (int(v) for v in mode[1:].rstrip("p").split("s"))
                 if tn > 2 * M and tn > 16:
                     continue
             us = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,

@@ -14,6 +14,7 @@ from paper_2402_10076_b200 import quick  # noqa: E402
 M, N, K = (int(v) for v in sys.argv[1:4])
 tn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 sk = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+FLAGS = int(os.environ.get("TRACE_FLAGS", "0"), 0)   # extra launch flags (e.g. 0x100000: CTA pair)
 G, TS, STRIDE = 128, 256, 8 + 7 * 256
 lib = quick.raw_library()
 lib.quick_debug_set_trace.argtypes = [ctypes.c_void_p]
@@ -24,11 +25,17 @@ x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((M, N), device="cuda", dtype=torch.float16)
 NCTA = quick.quick_gemm_plan(M, N, K, G)["num_ctas"] if not (tn or sk) else 4096
 tr = torch.zeros(16 * STRIDE + 3 * max(NCTA, 4096), dtype=torch.int64, device="cuda")
+
+
+def run(w):
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), w.data_ptr(), M, N, K, G, y.data_ptr(), 0, FLAGS, tn, sk)
+
+
 for i in range(3):
-    quick.quick_w4a16_gemm(x, copies[i], N, K, G, out=y, tile_n=tn, split_k=sk)
+    run(copies[i])
 torch.cuda.synchronize()
 lib.quick_debug_set_trace(ctypes.c_void_p(tr.data_ptr()))
-quick.quick_w4a16_gemm(x, copies[-1], N, K, G, out=y, tile_n=tn, split_k=sk)
+run(copies[-1])
 torch.cuda.synchronize()
 lib.quick_debug_set_trace(ctypes.c_void_p(0))
 tt = tr.cpu().numpy()
