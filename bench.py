@@ -28,6 +28,10 @@ import time
 
 import numpy as np
 
+# debug/ablation only: extra internal launch flags OR-ed into the timed launches (e.g. 0x80000 =
+# automatic plan without CTA pairs); 0 for every reported number
+EXTRA_FLAGS = int(os.environ.get("QUICK_BENCH_EXTRA_FLAGS", "0"), 0)
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -194,7 +198,7 @@ def run_quick(args, rank, world, dist):
     def launch(g, slot):
         x = g["xs"][slot % len(g["xs"])]
         quick.quick_w4a16_gemm_raw(x.data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nr"], g["K"], G,
-                                   g["y"].data_ptr(), sh, flags=quick.QUICK_FLAG_PDL)
+                                   g["y"].data_ptr(), sh, flags=quick.QUICK_FLAG_PDL | EXTRA_FLAGS)
 
     for g in gemms:   # eager first: allocates the stream-K workspace outside graph capture
         launch(g, 0)

@@ -58,6 +58,7 @@ constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no 
 constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
 constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memory (Cfg AM = 1)
 constexpr int kForcePair = 1 << 20;        // debug: CTA-pair (cta_group::2) plan for tiles 128/256
+constexpr int kDebugNoPair = 1 << 19;      // debug: automatic plan without CTA pairs
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -163,9 +164,11 @@ struct Seg {
   int tile, t, mt, a_lo, a_hi;
 };
 
-// Enumerates this CTA's segments.  Cluster split-K: exactly one (blockIdx.y, blockIdx.z, the
+// Enumerates this CTA's segments.  Cluster split-K: exactly one (n-tile blockIdx.z, m-tile
+// blockIdx.y -- the m-tiles of one n-tile are launched next to each other, so the CTAs reading
+// the same weights run in the same wave and all but the first read them from L2 -- and the
 // split's A range).  Stream-K: the unit range of CTA blockIdx.x, cut at tile boundaries.
-// CTA pairs: blockIdx.x = 2 x split + member, n-tile 2 blockIdx.y + member.
+// CTA pairs: blockIdx.x = 2 x split + member, n-tile 2 blockIdx.z + member.
 struct SegIter {
   int u, u1;
   int NA, m_tiles;
@@ -183,8 +186,8 @@ struct SegIter {
     } else {
       const int S = pair ? (int)gridDim.x >> 1 : (int)gridDim.x;
       const int sp = pair ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
-      t = pair ? 2 * (int)blockIdx.y + ((int)blockIdx.x & 1) : (int)blockIdx.y;
-      mt = blockIdx.z;
+      t = pair ? 2 * (int)blockIdx.z + ((int)blockIdx.x & 1) : (int)blockIdx.z;
+      mt = blockIdx.y;
       a_lo = (int)(((long long)sp * NA) / S);
       a_hi = (int)(((long long)(sp + 1) * NA) / S);
       u = u1 = 0;
@@ -404,8 +407,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   }
   // debug tracing (TRACE instantiation only, tools/trace_gemm.py): clock64 stamps per stage
   unsigned long long* tr = nullptr;
-  const unsigned lin16 = SK ? blockIdx.x : blockIdx.y * gridDim.x + blockIdx.x;
-  if (TRACE && blockIdx.z == 0 && lin16 < 16) tr = p.trace + (size_t)lin16 * kTraceStride;
+  const unsigned lin16 = SK ? blockIdx.x : blockIdx.z * gridDim.x + blockIdx.x;
+  if (TRACE && blockIdx.y == 0 && lin16 < 16) tr = p.trace + (size_t)lin16 * kTraceStride;
   auto stamp = [&](int ev, int i) {
     if (TRACE && tr != nullptr && i < kTraceStages) tr[8 + ev * kTraceStages + i] = clock64();
   };
@@ -1004,7 +1007,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[5] = clock64();
     ptx::cluster_sync();
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[6] = clock64();
-    const int m0 = blockIdx.z * BN;
+    const int m0 = blockIdx.y * BN;
     const uint32_t my = PAIR ? (crank >> 1) : ptx::cluster_ctarank();   // split index
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
     const int eb = (int)(((int)my * E4) / S) * 4;
@@ -1030,7 +1033,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         }
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
-      const int tt = PAIR ? 2 * (int)blockIdx.y + (int)member : (int)blockIdx.y;
+      const int tt = PAIR ? 2 * (int)blockIdx.z + (int)member : (int)blockIdx.z;
       const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * kTileRows + rr;
       if (out_fp32) {
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
@@ -1461,7 +1464,8 @@ int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
 //    keeps >= 2 A stages;
 //  - always S >= ceil(K / 8192) for accuracy (a TMEM accumulator sums at most 8192 of K,
 //    DESIGN.md R15).
-Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bool allow_sk) {
+Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bool allow_sk,
+                 bool allow_pair = true) {
   (void)G;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
@@ -1500,7 +1504,7 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
       if (tc == 256 && M <= 128) continue;
       const int mt = (M + tc - 1) / tc;
       for (int pr = 0; pr < 2; ++pr) {
-        if (pr && n_tiles % 2 != 0) continue;
+        if (pr && (n_tiles % 2 != 0 || !allow_pair)) continue;
         for (int s2 = 1; s2 <= (pr ? quick::kMaxSplit / 2 : quick::kMaxSplit); ++s2) {
           if (s2 < s_min) continue;
           if (s2 > 1 && s2 > NA / 2) break;
@@ -1552,7 +1556,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   if (SK)
     cfg.gridDim = dim3((unsigned)P, 1, 1);
   else
-    cfg.gridDim = dim3((unsigned)S, (unsigned)kp.n_tiles, (unsigned)kp.m_tiles);
+    cfg.gridDim = dim3((unsigned)S, (unsigned)kp.m_tiles, (unsigned)kp.n_tiles);   // m-tiles adjacent
   cfg.blockDim = dim3((unsigned)C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   if (kp.flags & quick::kDebugOneCta) cfg.dynamicSmemBytes = std::max<size_t>(C::SMEM_BYTES, 120 * 1024);
@@ -1586,7 +1590,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
                                             : quick::quick_w4a16_tc_kernel<BN, false, false, false, 2>);
       e = cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::SMEM_BYTES);
       if (e != cudaSuccess) return cuda_fail(e);
-      cfg.gridDim = dim3((unsigned)(2 * S), (unsigned)(kp.n_tiles / 2), (unsigned)kp.m_tiles);
+      cfg.gridDim = dim3((unsigned)(2 * S), (unsigned)kp.m_tiles, (unsigned)(kp.n_tiles / 2));
       cfg.dynamicSmemBytes = CP::SMEM_BYTES;
       cfg.blockDim = dim3((unsigned)CP::THREADS, 1, 1);
       na = 0;
@@ -1686,7 +1690,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
                     quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly | quick::kAblationSmemA | quick::kForcePair;
+                    quick::kDebugPdlEarly | quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1695,7 +1699,8 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
 
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
   Plan plan = choose_plan(M, N, K, G, tile_n, split_k,
-                          (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0);
+                          (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0,
+                          (flags & quick::kDebugNoPair) == 0);
   if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
   if ((flags & quick::kForcePair) && !plan.sk && plan.tile_n >= 128 && (N / quick::kTileRows) % 2 == 0 &&
       2 * plan.split <= quick::kMaxSplit)
