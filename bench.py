@@ -296,6 +296,7 @@ def run_quick(args, rank, world, dist):
                       "frac_tensor": round(tfl / peaks["tflops"], 4),
                       "bound": "tensor" if fl / by >= ridge else "hbm",
                       "tile_n": g["plan"]["tile_n"], "split_k": g["plan"]["split_k"],
+                      "cta_pair": g["plan"].get("pair", False),
                       "ctas": g["plan"]["num_ctas"]})
     layer_stack = None
     if args.workload == "mistral7b_stack":
@@ -315,7 +316,8 @@ def run_quick(args, rank, world, dist):
                 "frac": round(d["gbs"] / peaks["hbm_gbs"], 4)}
     tkey = f"{args.workload}:{d['N']}:{d['K']}:{d['M']}"
     roof["traffic"] = traffic.get(tkey)
-    roof["kernel"] = f"quick_w4a16_tc_kernel<{d['tile_n']}> M={d['M']} N={d['N']} K={d['K']} split_k={d['split_k']}"
+    roof["kernel"] = (f"quick_w4a16_tc_kernel<{d['tile_n']}{', cta_group::2 pair' if d.get('cta_pair') else ''}> "
+                      f"M={d['M']} N={d['N']} K={d['K']} split_k={d['split_k']}")
     roof["algorithmic_per_launch"] = algo_bytes(d["M"], d["N"], d["K"], G) if d["bound"] == "hbm" else \
         algo_flops(d["M"], d["N"], d["K"])
     roof["peak_source"] = peaks["source"]
