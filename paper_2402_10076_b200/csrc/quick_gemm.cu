@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/quick.h"
@@ -1026,23 +1027,19 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 #pragma unroll
     for (int q = 0; q < kMaxSplit; ++q)   // (pair: the same member of each split's pair)
       peer[q] = ptx::mapa(sbase, PAIR ? (uint32_t)(2 * (q < S ? q : 0)) + member : (uint32_t)(q < S ? q : 0));
-    for (int e = eb + (int)threadIdx.x * 4; e < e_lim; e += kThreads * 4) {
-      float4 v[kMaxSplit];
-#pragma unroll
-      for (int q = 0; q < kMaxSplit; ++q)
-        if (q < S) v[q] = ptx::ld_dsmem_f32x4(peer[q] + (uint32_t)e * 4u);
-      float4 acc = v[0];
-#pragma unroll
-      for (int q = 1; q < kMaxSplit; ++q)
-        if (q < S) {
-          acc.x += v[q].x;
-          acc.y += v[q].y;
-          acc.z += v[q].z;
-          acc.w += v[q].w;
-        }
+    const int tt = PAIR ? 2 * (int)blockIdx.z + (int)member : (int)blockIdx.z;
+    // partial q of element e (float4 index): our own through ld.shared, the others' through DSMEM
+    auto load_part = [&](int q, int e) {
+      if (q == (int)my) {
+        const uint4 u = ptx::lds128(sbase + (uint32_t)e * 4u);
+        return make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                           __uint_as_float(u.w));
+      }
+      return ptx::ld_dsmem_f32x4(peer[q] + (uint32_t)e * 4u);
+    };
+    auto store_sum = [&](int e, const float4& acc) {
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
-      const int tt = PAIR ? 2 * (int)blockIdx.z + (int)member : (int)blockIdx.z;
       const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * kTileRows + rr;
       if (out_fp32) {
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
@@ -1053,6 +1050,59 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
         *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
+      }
+    };
+    // The reduce is latency-bound (a DSMEM load takes ~500 cycles): for S <= 4 each thread keeps
+    // UNR elements x S loads in flight before the first add.  Sum order q = 0..S-1 throughout.
+    auto reduce_unrolled = [&](auto s_const) {
+      constexpr int SS = decltype(s_const)::value;
+      constexpr int UNR = SS <= 2 ? 4 : 2;
+      constexpr int kStride = kThreads * 4;
+      for (int e0 = eb + (int)threadIdx.x * 4; e0 < e_lim; e0 += kStride * UNR) {
+        float4 v[UNR][SS];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          if (e0 + u * kStride < e_lim) {
+#pragma unroll
+            for (int q = 0; q < SS; ++q) v[u][q] = load_part(q, e0 + u * kStride);
+          }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          if (e0 + u * kStride < e_lim) {
+            float4 acc = v[u][0];
+#pragma unroll
+            for (int q = 1; q < SS; ++q) {
+              acc.x += v[u][q].x;
+              acc.y += v[u][q].y;
+              acc.z += v[u][q].z;
+              acc.w += v[u][q].w;
+            }
+            store_sum(e0 + u * kStride, acc);
+          }
+      }
+    };
+    if (S == 2) {
+      reduce_unrolled(std::integral_constant<int, 2>{});
+    } else if (S == 3) {
+      reduce_unrolled(std::integral_constant<int, 3>{});
+    } else if (S == 4) {
+      reduce_unrolled(std::integral_constant<int, 4>{});
+    } else {
+      for (int e = eb + (int)threadIdx.x * 4; e < e_lim; e += kThreads * 4) {
+        float4 v[kMaxSplit];
+#pragma unroll
+        for (int q = 0; q < kMaxSplit; ++q)
+          if (q < S) v[q] = load_part(q, e);
+        float4 acc = v[0];
+#pragma unroll
+        for (int q = 1; q < kMaxSplit; ++q)
+          if (q < S) {
+            acc.x += v[q].x;
+            acc.y += v[q].y;
+            acc.z += v[q].z;
+            acc.w += v[q].w;
+          }
+        store_sum(e, acc);
       }
     }
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[7] = clock64();
