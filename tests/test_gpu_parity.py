@@ -406,20 +406,23 @@ def test_ablation_smem_a_bit_identical(M, N, K, tn, sk):
 PAIR = 1 << 20   # internal flag: force the CTA-pair (cta_group::2) variant of a tile-128/256 plan
 
 
-@pytest.mark.parametrize("M,N,K,tn,sk", [(256, 512, 512, 256, 1), (200, 256, 1024, 128, 1), (130, 768, 1280, 128, 3),
-                                         (300, 512, 2048, 256, 2), (97, 1024, 640, 128, 4), (256, 256, 384, 256, 3)])
-def test_pair_bit_identical_and_oracle(M, N, K, tn, sk):
+@pytest.mark.parametrize("M,N,K,tn,sk,G", [(256, 512, 512, 256, 1, 128), (200, 256, 1024, 128, 1, 128),
+                                           (130, 768, 1280, 128, 3, 128), (300, 512, 2048, 256, 2, 128),
+                                           (97, 1024, 640, 128, 4, 128), (256, 256, 384, 256, 3, 128),
+                                           (200, 512, 704, 256, 2, 64), (129, 256, 576, 128, 2, 32)])
+def test_pair_bit_identical_and_oracle(M, N, K, tn, sk, G):
     """CTA pairs (M = 256 MMAs over two SMs, X split by tokens between the pair):
     the same MMAs in the same K order as one CTA per n-tile, so bit-identical to the ordinary plan
     of that tile/split, and within tolerance of the oracle.  Ragged M, ragged K (K % 128 = 64),
-    odd A-stage splits and one-cluster-of-8 (S = 4) cases."""
-    p = synth.make_problem(M + K + 7, M=M, N=N, K=K, G=128)
+    odd A-stage splits, one-cluster-of-8 (S = 4) cases, and K % 128 = 64 with small groups (the
+    general group path)."""
+    p = synth.make_problem(M + K + 7, M=M, N=N, K=K, G=G)
     x, blob = to_dev_f16(p.x), pack_dev(p)
     y0 = torch.full((M, N), float("nan"), device=DEV, dtype=torch.float16)
     y1 = torch.full((M, N), float("nan"), device=DEV, dtype=torch.float16)
     h = torch.cuda.current_stream().cuda_stream
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y0.data_ptr(), h, 0, tn, sk)
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y1.data_ptr(), h, PAIR, tn, sk)
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y0.data_ptr(), h, 0, tn, sk)
+    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y1.data_ptr(), h, PAIR, tn, sk)
     torch.cuda.synchronize()
     assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
     check_tol(p, y1)
