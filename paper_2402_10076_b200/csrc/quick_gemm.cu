@@ -906,9 +906,56 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           ptx::tmem_wait_ld();
         }
       };
+      // 32 accumulator columns with one tcgen05.wait::ld (4 loads in flight: the epilogue was a
+      // chain of load -> wait round trips, ~9000 cycles per CTA for the 256-token tile)
+      constexpr bool kLd32 = C::NACC == 1 && kColsPerWarp % 32 == 0;
+      auto load_d32 = [&](int jc, uint32_t (&v)[32]) {
+        uint32_t a0[8], a1[8], a2[8], a3[8];
+        ptx::tmem_ld_32x32b_x8(dcol + jc, a0);
+        ptx::tmem_ld_32x32b_x8(dcol + jc + 8, a1);
+        ptx::tmem_ld_32x32b_x8(dcol + jc + 16, a2);
+        ptx::tmem_ld_32x32b_x8(dcol + jc + 24, a3);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[i] = a0[i];
+          v[8 + i] = a1[i];
+          v[16 + i] = a2[i];
+          v[24 + i] = a3[i];
+        }
+      };
       const bool whole = SK ? (sg.a_lo == 0 && sg.a_hi == p.NA) : (S == 1);
       const int jmax = min(jend, M - m0);   // valid tokens (columns)
-      if (whole) {
+      if (whole && kLd32) {
+        // column i of the chunk is token m0 + jc + i: one store per token at a running pointer
+        // (row stride ldy), the output type and the full-chunk test hoisted out of the loop (the
+        // per-element 64-bit index math and branches made this epilogue instruction-bound)
+#pragma unroll 1
+        for (int jc = j0; jc < jmax; jc += 32) {
+          uint32_t v[32];
+          load_d32(jc, v);
+          const int cnt = jmax - jc;   // valid tokens in this chunk (>= 32: all)
+          // (the pointer is made opaque after each bump so that the compiler does not keep 32
+          // precomputed 64-bit addresses live)
+          if (out_fp32) {
+            float* yp = reinterpret_cast<float*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < cnt) *yp = __uint_as_float(v[i]);
+              yp += p.ldy;
+              asm volatile("" : "+l"(yp));
+            }
+          } else {
+            __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (i < cnt) *yp = __float2half_rn(__uint_as_float(v[i]));
+              yp += p.ldy;
+              asm volatile("" : "+l"(yp));
+            }
+          }
+        }
+      } else if (whole) {
         // the full K range of this tile is in our accumulator: straight to Y
 #pragma unroll 1
         for (int jc = j0; jc < jmax; jc += 8) {
@@ -925,6 +972,16 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
                 reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(f);
             }
           }
+        }
+      } else if (!SK && kLd32) {
+        // cluster split-K: fp32 partial tile [BN][128] into our shared memory (as below)
+#pragma unroll 1
+        for (int jc = j0; jc < jend; jc += 32) {
+          uint32_t v[32];
+          load_d32(jc, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            ptx::sts_u32(sbase + (uint32_t)(((jc + i) * kTileRows + r) * 4), v[i]);
         }
       } else if (!SK) {
         // cluster split-K: fp32 partial tile [BN][128] into our shared memory (pipeline buffers
@@ -1007,6 +1064,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         ptx::mbar_arrive(bar_dempty + 8 * db);
       }
       ++si;
+      if (TRACE && tr != nullptr && warp == 0 && lane == 0 && whole && !SK) tr[5] = clock64();
     }
   }
 
@@ -1113,6 +1171,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 
   ptx::tc_fence_before();
   __syncthreads();
+  if (TRACE && tr != nullptr && threadIdx.x == 0 && S == 1 && !SK) tr[6] = clock64();
   if (TRACE && threadIdx.x == 0) {
     // all CTAs: (smid, start ns, end ns) after the 16 detailed records
     unsigned long long t_end_ns;
