@@ -924,6 +924,26 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           v[24 + i] = a3[i];
         }
       };
+      // 8 tokens (columns jc .. jc + 7, the first `cnt` valid) of this thread's output column n
+      auto store_y8 = [&](int jc, const float (&f)[8], int cnt) {
+        if (out_fp32) {
+          float* yp = reinterpret_cast<float*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < cnt) *yp = f[i];
+            yp += p.ldy;
+            asm volatile("" : "+l"(yp));
+          }
+        } else {
+          __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < cnt) *yp = __float2half_rn(f[i]);
+            yp += p.ldy;
+            asm volatile("" : "+l"(yp));
+          }
+        }
+      };
       const bool whole = SK ? (sg.a_lo == 0 && sg.a_hi == p.NA) : (S == 1);
       const int jmax = min(jend, M - m0);   // valid tokens (columns)
       if (whole && kLd32) {
@@ -961,17 +981,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         for (int jc = j0; jc < jmax; jc += 8) {
           uint32_t v[8];
           load_d(jc, v);
+          float f[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int m = m0 + jc + i;
-            if (m < M) {
-              const float f = __uint_as_float(v[i]);
-              if (out_fp32)
-                reinterpret_cast<float*>(p.Y)[(size_t)m * p.ldy + n] = f;
-              else
-                reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(f);
-            }
-          }
+          for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(v[i]);
+          store_y8(jc, f, jmax - jc);
         }
       } else if (!SK && kLd32) {
         // cluster split-K: fp32 partial tile [BN][128] into our shared memory (as below)
@@ -1044,16 +1057,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 #pragma unroll
               for (int i = 0; i < 8; ++i) acc[i] += pv[i];
             }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int m = m0 + jc + i;
-              if (jc + i < jmax) {
-                if (out_fp32)
-                  reinterpret_cast<float*>(p.Y)[(size_t)m * p.ldy + n] = acc[i];
-                else
-                  reinterpret_cast<__half*>(p.Y)[(size_t)m * p.ldy + n] = __float2half_rn(acc[i]);
-              }
-            }
+            store_y8(jc, acc, jmax - jc);
           }
           ptx::tc_fence_before();
           ptx::mbar_arrive(bar_dempty + 8 * db);
