@@ -1634,7 +1634,12 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
           const int res = pr ? max_resident_pair(tc, s2) : max_resident(tc, false, s2);
           const long long waves = (units + res - 1) / res;
           const int csz = s2 * (pr ? 2 : 1);
-          const double t = (double)waves * (((NA + s2 - 1) / s2) * st[tc == 256][pr] + fixed[tc == 256][pr] +
+          // a tile-128 pair grid that fits one CTA per SM runs each CTA alone on its SM (the
+          // fitted 0.648 us is for two co-resident pairs): 0.426 us per stage, measured at 4096^2
+          // M = 192/256, S = 2 (12.5 us vs 13.2 for one CTA per n-tile)
+          const bool alone = pr && tc == 128 && units * 2 * s2 <= sm_count();
+          const double t = (double)waves * (((NA + s2 - 1) / s2) * (alone ? 0.426 : st[tc == 256][pr]) +
+                                            fixed[tc == 256][pr] +
                                             (s2 > 1 ? 1.933 : 0.0) + 0.355 * (csz - 1) + (csz == 8 ? 1.209 : 0.0));
           if (t < best) {
             best = t;
