@@ -89,6 +89,9 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
  *   tile_n    tokens per MMA tile (16, 32, 64, 128, 256), 0 = automatic
  *   split_k   CTAs per cluster splitting K (1..8, <= ceil(K/128)), 0 = automatic (which may
  *             choose stream-K for tiles <= 64)
+ * With tile_n = split_k = 0 and M > 64 the automatic plan may run tiles of 128/256 tokens as CTA
+ * pairs (tcgen05 cta_group::2: two n-tiles per cluster of two SMs); a forced
+ * (tile_n, split_k) runs one CTA per n-tile.  Both compute the same MMAs in the same K order.
  * Deterministic: equal inputs and equal (tile_n, split_k) give bit-equal Y. */
 quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K,
                                    int group_size, void* Y, int ldy, int flags, int tile_n,
