@@ -189,8 +189,8 @@ struct SegIter {
       const int sp = pair ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
       t = pair ? 2 * (int)blockIdx.z + ((int)blockIdx.x & 1) : (int)blockIdx.z;
       mt = blockIdx.y;
-      a_lo = (int)(((long long)sp * NA) / S);
-      a_hi = (int)(((long long)(sp + 1) * NA) / S);
+      a_lo = (sp * NA) / S;          // 32-bit: S <= 8 and NA = ceil(K / 128) < 2^27
+      a_hi = ((sp + 1) * NA) / S;
       u = u1 = 0;
     }
   }
@@ -354,22 +354,22 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   // Prologue.  The producer initialises the barriers and starts loading at once; the other
   // warps wait on named barrier 2 (which orders the inits before them) while the MMA warp
   // allocates TMEM, so the first loads are not held up by the allocation.
-  if (threadIdx.x == kProducerWarp * 32) {
-    for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(bar_full + 8 * s, 1);
-      ptx::mbar_init(bar_xfull + 8 * s, 1);
-      // 128 dequant-thread arrivals per A stage of the load stage (a thread reading the only A
-      // stage of a short load stage arrives for both) + 1 MMA commit
-      ptx::mbar_init(bar_empty + 8 * s, 4 * 32 * APL + 1);
-    }
-    for (int a = 0; a < kAStages; ++a) {
-      // every thread of one parity group (CTA pair: one arrival per warp of both members)
-      ptx::mbar_init(bar_afull + 8 * a, kWarpArrive ? (PAIR ? 8 : 4) : 4 * 32);
-      ptx::mbar_init(bar_aempty + 8 * a, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(bar_dfull + 8 * b, 1);
-      ptx::mbar_init(bar_dempty + 8 * b, kDqThreads);
+  if (warp == kProducerWarp) {
+    // one barrier per lane (the barriers are contiguous from BAR_OFF: full[STAGES],
+    // empty[STAGES], afull[A], aempty[A], dfull[2], dempty[2], xfull[STAGES]); a serial init of
+    // ~20 barriers by one thread delayed every warp's start
+    static_assert(C::NUM_BARS <= 32, "one barrier per producer lane");
+    if (lane < C::NUM_BARS) {
+      const int i = lane;
+      uint32_t cnt = 1;   // full, aempty, dfull, xfull
+      if (i >= STAGES && i < 2 * STAGES)
+        cnt = 4 * 32 * APL + 1;   // empty: 128 dequant-thread arrivals per A stage (a thread reading
+                                  // the only A stage of a short load stage arrives for both) + 1 commit
+      else if (i >= 2 * STAGES && i < 2 * STAGES + kAStages)   // afull: one parity group (CTA pair:
+        cnt = kWarpArrive ? (PAIR ? 8 : 4) : 4 * 32;          // one arrival per warp of both members)
+      else if (i >= 2 * STAGES + 2 * kAStages + 2 && i < 2 * STAGES + 2 * kAStages + 4)
+        cnt = kDqThreads;         // dempty
+      ptx::mbar_init(bar_full + 8 * i, cnt);
     }
     ptx::fence_mbar_init();
   }
