@@ -60,6 +60,7 @@ constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the
 constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memory (Cfg AM = 1)
 constexpr int kForcePair = 1 << 20;        // debug: CTA-pair (cta_group::2) plan for tiles 128/256
 constexpr int kDebugNoPair = 1 << 19;      // debug: automatic plan without CTA pairs
+constexpr int kDebugForceSk = 1 << 17;     // debug: stream-K whenever the tile allows it
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -1587,7 +1588,7 @@ int cover_tile(int M) { return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : 128;
 //  - always S >= ceil(K / 8192) for accuracy (a TMEM accumulator sums at most 8192 of K,
 //    DESIGN.md R15).
 Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bool allow_sk,
-                 bool allow_pair = true) {
+                 bool allow_pair = true, bool force_sk = false) {
   (void)G;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
@@ -1604,7 +1605,12 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
     // reduce is cheaper than the workspace fix-up (measured on B200: 4096^2 and both 13B
     // shapes favour the cluster, 28672x8192 stream-K)
     // (a segment never spans more than one tile, so the accuracy cap only binds when NA > cap)
-    if (2 * (U / P) >= NA && (NA <= kMaxAccumK / quick::kKA || (U + P - 1) / P <= kMaxAccumK / quick::kKA))
+    // (tiles <= 32: up to ~5 contributors per tile still pay -- measured on B200 with the debug
+    // flag kDebugForceSk: 13824x5120 M <= 16 13.2 vs 13.8 us, 8192x28672 M <= 32 31.1 vs 32.9;
+    // 7-8 contributors lose: 5120x13824, 4096^2; tile 64 keeps the half-tile rule)
+    const long long reach = tn <= 32 ? 5 : 2;
+    if ((force_sk || reach * (U / P) >= NA) &&
+        (NA <= kMaxAccumK / quick::kKA || (U + P - 1) / P <= kMaxAccumK / quick::kKA))
       return Plan{tn, 1, (int)P, true, (int)P};
   }
   const int s_min = (K + kMaxAccumK - 1) / kMaxAccumK;
@@ -1817,7 +1823,8 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
                     quick::kDebugExitTop | quick::kDebugExitPrologue |
                     quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly | quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair;
+                    quick::kDebugPdlEarly | quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair |
+                    quick::kDebugForceSk;
   if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1827,7 +1834,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
   Plan plan = choose_plan(M, N, K, G, tile_n, split_k,
                           (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0,
-                          (flags & quick::kDebugNoPair) == 0);
+                          (flags & quick::kDebugNoPair) == 0, (flags & quick::kDebugForceSk) != 0);
   if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
   if ((flags & quick::kForcePair) && !plan.sk && plan.tile_n >= 128 && (N / quick::kTileRows) % 2 == 0 &&
       2 * plan.split <= quick::kMaxSplit)

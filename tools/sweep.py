@@ -34,6 +34,7 @@ torch.cuda.set_stream(stream)
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
 L = 16
 FLAGS = {"auto": 0, "pdl": quick.QUICK_FLAG_PDL, "nosk": quick.QUICK_FLAG_NO_STREAMK,
+         "sk": quick.QUICK_FLAG_PDL | (1 << 17),   # debug: stream-K whenever the tile allows it
          "pdlearly": quick.QUICK_FLAG_PDL | (1 << 24)}
 
 
