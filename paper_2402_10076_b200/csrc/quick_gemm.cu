@@ -359,9 +359,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     // one barrier per lane (the barriers are contiguous from BAR_OFF: full[STAGES],
     // empty[STAGES], afull[A], aempty[A], dfull[2], dempty[2], xfull[STAGES]); a serial init of
     // ~20 barriers by one thread delayed every warp's start
-    static_assert(C::NUM_BARS <= 32, "one barrier per producer lane");
-    if (lane < C::NUM_BARS) {
-      const int i = lane;
+    for (int i = lane; i < C::NUM_BARS; i += 32) {
       uint32_t cnt = 1;   // full, aempty, dfull, xfull
       if (i >= STAGES && i < 2 * STAGES)
         cnt = 4 * 32 * APL + 1;   // empty: 128 dequant-thread arrivals per A stage (a thread reading
