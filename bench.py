@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """bench.py -- W4A16 GEMM throughput on B200 vs roofline (BASELINE.json metric).
 
-A *step* is one pass of the hot path over the workload's GEMM list; for the default workload
-(BASELINE.json configs[1], Llama-2-7B attention projection N = K = 4096, g128) that is the
-M sweep 1, 2, 4, ..., 256: nine quick_w4a16_gemm launches on synthetic AWQ weights.
+A *step* is one pass of the hot path over the workload's GEMM list.  The default workload is the
+one the metric ("M=1-1024, 1/2/4/8 B200") is quoted on, BASELINE.json configs[3]: the Llama-2-70B
+MLP pair, the up-projection 28672x8192 (K=8192 -> N=28672, column-parallel) and the
+down-projection 8192x28672 (K=28672 -> N=8192, row-parallel), g128, each at
+M = 1, 4, 16, 64, 128, 256, 512, 1024: sixteen quick_w4a16_gemm_ex launches on synthetic AWQ
+weights.  Other configs: --workload llama2_7b_attn (configs[1]), llama2_13b_mlp (configs[2]),
+mistral7b_stack (configs[4]), tiny (configs[0]), paper_fig7 (the paper's 8192x8192 sweep).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl quick|reference] [--workload W]
 
-Timing: weights are packed offline once (host, C++), then R device copies of the
-blob rotate launch by launch so every launch streams its weights from HBM (R copies > 2.5 x L2),
-never from L2.  The K timed steps run as CUDA-graph replays, M-major in blocks of C steps (graph
-per M point holding C launches), with CUDA events on the launching stream between graph
-replays, so the per-M average launch duration is measured over the whole timed region.
-`value` = whole-job TFLOP/s (2 M N K per GEMM, all ranks) over the max-over-ranks device time.
-`e2e`  = same metric through the C-ABI with HOST buffers: every step copies X from pinned host
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run with
+N ranks (127.0.0.1); under torchrun WORLD_SIZE must equal N.
+
+Timing: weights are packed offline once (host, C++), then R device copies of each
+blob rotate launch by launch so every launch streams its weights from HBM (R copies > 2.5 x L2).
+The K timed steps run as CUDA-graph replays, GEMM-point-major in blocks of C steps, with CUDA events
+on the launching stream between replays, so each point's mean launch duration is measured over the
+whole timed region.  `value` = whole-job TFLOP/s (2 M N K per GEMM, all ranks) over the
+max-over-ranks device time.  Launches use QUICK_FLAG_PDL and a caller-owned stream-K workspace.
+`e2e` = the same metric through the C-ABI with HOST buffers: every step copies X from pinned host
 memory and Y back to pinned host memory inside the timed region (weights stay resident).
-N > 1: tensor parallel, weights column-sharded along N (multiples of 128), each rank runs the
-GEMM on its shard, then NCCL all-gather + quick_gather_columns materialise Y (strong scaling).
+N > 1: tensor parallel (strong scaling); column-parallel GEMMs shard N (multiples of 128) and
+all-gather Y (NCCL) + quick_gather_columns; row-parallel GEMMs shard K (group-aligned), write fp32
+partials, all-reduce them in fp32 (NCCL) + quick_f32_to_f16.  GEMM-only and GEMM+collective
+times are reported separately.
 """
 import argparse
 import json
@@ -38,15 +47,23 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402  (seeded random bits only)
 
 WORKLOADS = {
-    # name: (BASELINE.json config index, list of (N, K) shapes, M points, G)
-    "llama2_7b_attn": (1, [(4096, 4096)], [1, 2, 4, 8, 16, 32, 64, 128, 256], 128),
-    "llama2_13b_mlp": (2, [(13824, 5120), (5120, 13824)], [1, 2, 4, 8, 16, 32, 64, 128, 256, 512], 128),
-    "llama2_70b_mlp": (3, [(28672, 8192)], [1, 16, 64, 128, 256, 512, 1024], 128),
-    "tiny": (0, [(256, 512)], [8], 128),
-    # BASELINE.json configs[4]: one Mistral-7B decoder layer's linear stack (QKV, O, gate_up, down);
-    # tokens/s = M / (32 layers x the 4 GEMMs' time); attention, norms and SiLU are not on the path
-    "mistral7b_stack": (4, [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)], [1, 16, 64, 256], 128),
+    # name: (BASELINE.json config index, list of (N, K, tp kind) shapes, M points, G);
+    # tp kind "col" = column-parallel (N sharded), "row" = row-parallel (K sharded, fp32 all-reduce)
+    "llama2_70b_mlp": (3, [(28672, 8192, "col"), (8192, 28672, "row")], [1, 4, 16, 64, 128, 256, 512, 1024], 128),
+    "llama2_7b_attn": (1, [(4096, 4096, "col")], [1, 2, 4, 8, 16, 32, 64, 128, 256], 128),
+    "llama2_13b_mlp": (2, [(13824, 5120, "col"), (5120, 13824, "row")], [1, 2, 4, 8, 16, 32, 64, 128, 256, 512],
+                       128),
+    "tiny": (0, [(256, 512, "col")], [8], 128),
+    # BASELINE.json configs[4]: one Mistral-7B decoder layer's linear stack (QKV, O, gate_up, down) in the
+    # Megatron split: QKV and gate_up column-parallel (their sharded outputs feed the next GEMM, so no
+    # gather), O and down row-parallel (fp32 all-reduce); tokens/s = M / (32 layers x the 4 GEMMs' time);
+    # attention, norms and SiLU are not on the path
+    "mistral7b_stack": (4, [(6144, 4096, "colx"), (4096, 4096, "row"), (28672, 4096, "colx"), (4096, 14336, "row")],
+                        [1, 16, 64, 256], 128),
+    # the paper's kernel benchmark shape (Fig. 7): 8192 x 8192, batch 64 .. 512 (context)
+    "paper_fig7": (None, [(8192, 8192, "col")], [1, 16, 64, 128, 256, 512], 128),
 }
+DEFAULT_WORKLOAD = "llama2_70b_mlp"
 METRIC = "W4A16 GEMM TFLOP/s & HBM GB/s vs roofline, M=1–1024, 1/2/4/8 B200"
 BLOCK_C = 32  # steps per graph replay (M-major): PDL overlaps consecutive launches inside a graph
 
@@ -137,9 +154,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ GPU arm
+def plan_key(plan):
+    """Kernel identity of a launch: the template instantiation and grid family it runs."""
+    sched = "stream-K" if plan["split_k"] == 0 else f"split{plan['split_k']}"
+    return f"tile{plan['tile_n']}{'-pair' if plan['pair'] else ''}-{sched}"
+
+
 def run_quick(args, rank, world, dist):
     import torch
-    from paper_2402_10076_b200 import quick
+    from paper_2402_10076_b200 import quick, tp
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
@@ -147,47 +170,55 @@ def run_quick(args, rank, world, dist):
     props = torch.cuda.get_device_properties(dev)
     l2 = int(getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20)
 
-    # ---- problem: per shape, synthetic AWQ weights, column shard for this rank, offline pack
-    gemms = []   # one entry per (shape, M): dict
-    shard_info = []
-    blobs = []
-    pack_s = 0.0
-    for si, (N, K) in enumerate(shapes):
-        assert N % (128 * world) == 0, "column shard must be a multiple of 128"
-        Nr = N // world
-        qw = synth.make_qweight(si, K, N)
-        sc = synth.make_scales(si, K, N, G)
-        zr = synth.make_zeros(si, K, N, G)
-        c0 = rank * Nr
+    # ---- problem: per shape, synthetic AWQ weights, this rank's shard, offline pack (host, C++)
+    layers, pack_s = [], 0.0
+    for si, (N, K, kind) in enumerate(shapes):
+        qw, sc, zr = synth.make_qweight(si, K, N), synth.make_scales(si, K, N, G), synth.make_zeros(si, K, N, G)
+        if world > 1 and kind in ("col", "colx"):
+            qw, sc, zr = tp.shard_awq_columns(qw, sc, zr, rank, world)
+            Nl, Kl = N // world, K
+        elif world > 1:
+            qw, sc, zr = tp.shard_awq_rows(qw, sc, zr, G, rank, world)
+            Nl, Kl = N, K // world
+        else:
+            Nl, Kl = N, K
         t0 = time.perf_counter()
-        blob = quick.quick_pack_weights(qw[:, c0 // 8:(c0 + Nr) // 8], sc[:, c0:c0 + Nr], zr[:, c0 // 8:(c0 + Nr) // 8], G)
+        blob = quick.quick_pack_weights(qw, sc, zr, G)
         pack_s += time.perf_counter() - t0
-        blobs.append(blob)
-        shard_info.append((N, K, Nr))
-    blob_bytes = max(b.size for b in blobs)
-    per_step_launches = len(shapes) * len(Ms)
-    # weight copies: reuse distance >= 2.5 x L2 and a multiple of the launches per graph block
-    # slot of launch c of GEMM gi inside a block = (gi * C + c) % R; R divides the launches per
-    # block so the reuse distance of every slot is exactly R launches (> 2.5 x L2 of weights)
-    launches_per_rep = per_step_launches * BLOCK_C
+        layers.append(dict(si=si, N=N, K=K, kind=kind, Nl=Nl, Kl=Kl, blob=blob))
+    blob_bytes = max(l_["blob"].size for l_ in layers)
+    launches_per_rep = len(layers) * len(Ms) * BLOCK_C
+    # weight copies: reuse distance >= 2.5 x L2 (slot of launch c of point gi = (gi * C + c) % R, R
+    # divides the launches per block, so every slot is reused exactly R launches later)
     R_min = max(1, int(np.ceil(2.5 * l2 / blob_bytes)))
     l2_cold = R_min <= launches_per_rep
     R = min(d for d in range(R_min, launches_per_rep + 1) if launches_per_rep % d == 0) if l2_cold \
         else launches_per_rep
     wcopies = {}
-    for si, blob in enumerate(blobs):
-        base = torch.from_numpy(blob).to(dev)
-        wcopies[si] = [base] + [base.clone() for _ in range(R - 1)]
-    # activations: per (shape, M) R copies too (cold), outputs per (shape, M)
-    for si, (N, K, Nr) in enumerate(shard_info):
-        for mi, M in enumerate(Ms):
-            x_host = synth.make_x(1000 + M, M, K)
+    for l_ in layers:
+        base = torch.from_numpy(l_["blob"]).to(dev)
+        wcopies[l_["si"]] = [base] + [base.clone() for _ in range(R - 1)]
+    ws = quick.workspace_for([(M, l_["Nl"], l_["Kl"]) for l_ in layers for M in Ms], G, dev)
+    ws_ptr, ws_bytes = ws.data_ptr(), ws.numel()
+
+    gemms = []   # one entry per (shape, M) point
+    for l_ in layers:
+        for M in Ms:
+            x_host = synth.make_x(1000 + M, M, l_["K"])
+            if world > 1 and l_["kind"] == "row":
+                k0, k1 = tp.row_shard_bounds(l_["K"], G, world, rank)
+                x_host = np.ascontiguousarray(x_host[:, k0:k1])
             xs = [torch.from_numpy(x_host.view(np.int16)).view(torch.float16).to(dev) for _ in range(min(R, 8))]
-            y = torch.empty((M, Nr), device=dev, dtype=torch.float16)
-            plan = quick.quick_gemm_plan(M, Nr, K, G)
-            gemms.append(dict(si=si, M=M, N=N, K=K, Nr=Nr, xs=xs, y=y, plan=plan, x_host=x_host,
-                              gathered=torch.empty((world, M, Nr), device=dev, dtype=torch.float16) if world > 1 else None,
-                              yfull=torch.empty((M, N), device=dev, dtype=torch.float16) if world > 1 else None))
+            row_partial = world > 1 and l_["kind"] == "row"
+            y = torch.empty((M, l_["Nl"]), device=dev, dtype=torch.float32 if row_partial else torch.float16)
+            g = dict(l_, M=M, xs=xs, y=y, x_host=x_host, plan=quick.quick_gemm_plan(M, l_["Nl"], l_["Kl"], G,
+                                                                                     workspace_bytes=ws_bytes))
+            if world > 1 and l_["kind"] == "col":
+                g["gathered"] = torch.empty((world, M, l_["Nl"]), device=dev, dtype=torch.float16)
+                g["yfull"] = torch.empty((M, l_["N"]), device=dev, dtype=torch.float16)
+            if row_partial:
+                g["yfull"] = torch.empty((M, l_["N"]), device=dev, dtype=torch.float16)
+            gemms.append(g)
 
     stream = torch.cuda.Stream(dev)        # graph capture needs a non-default stream
     torch.cuda.set_stream(stream)
@@ -197,51 +228,65 @@ def run_quick(args, rank, world, dist):
     # prologue and weight prefetch overlap the previous kernel's tail (X / Y stay ordered)
     def launch(g, slot):
         x = g["xs"][slot % len(g["xs"])]
-        quick.quick_w4a16_gemm_raw(x.data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nr"], g["K"], G,
-                                   g["y"].data_ptr(), sh, flags=quick.QUICK_FLAG_PDL | EXTRA_FLAGS)
+        fl = quick.QUICK_FLAG_PDL | EXTRA_FLAGS | (quick.QUICK_FLAG_OUT_F32 if g["y"].dtype == torch.float32 else 0)
+        quick.quick_w4a16_gemm_raw(x.data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nl"], g["Kl"], G,
+                                   g["y"].data_ptr(), sh, flags=fl, ws_ptr=ws_ptr, ws_bytes=ws_bytes)
 
-    for g in gemms:   # eager first: allocates the stream-K workspace outside graph capture
+    def collective(g):
+        if world == 1 or g["kind"] == "colx":
+            return          # colx: the sharded output feeds the next (row-parallel) GEMM, no gather
+        if g["kind"] == "col":   # all-gather the per-rank [M][Nr] slices, then permute to [M][N]
+            dist.all_gather_into_tensor(g["gathered"].view(-1), g["y"].view(-1))
+            quick.quick_gather_columns(g["gathered"], world, g["M"], g["Nl"], dst=g["yfull"])
+        else:                    # row: fp32 all-reduce of the partials, then cast
+            dist.all_reduce(g["y"], op=dist.ReduceOp.SUM)
+            quick.quick_f32_to_f16(g["y"], dst=g["yfull"])
+
+    for g in gemms:
         launch(g, 0)
+        collective(g)
     torch.cuda.synchronize()
 
-    # graph per (gemm index, block size C): C launches of that GEMM with rotating weight slots;
-    # launch index inside a rep = gi * C + c -> slot (gi * C + c) % R  (R divides gi-count * C)
-    def build_graphs(C):
+    # graph per GEMM point holding C launches (+ their collectives when `with_coll`)
+    def build_graphs(C, with_coll):
         graphs = []
         for gi, g in enumerate(gemms):
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=stream):
                 for c in range(C):
                     launch(g, (gi * C + c) % R)
+                    if with_coll:
+                        collective(g)
             graphs.append(gr)
         return graphs
 
-    def collective(g):
-        # column-parallel TP: all-gather the per-rank [M][Nr] slices, then permute to [M][N]
-        dist.all_gather_into_tensor(g["gathered"].view(-1), g["y"].view(-1))
-        quick.quick_gather_columns(g["gathered"], world, g["M"], g["Nr"], dst=g["yfull"])
-
     K_steps, W = args.steps, args.warmup
-    graphs_full = build_graphs(BLOCK_C)
+    coll_in_graph = world > 1
+    try:
+        graphs_full = build_graphs(BLOCK_C, coll_in_graph)
+    except Exception:        # a NCCL build that cannot be captured: collectives run eagerly
+        torch.cuda.synchronize()
+        coll_in_graph = False
+        graphs_full = build_graphs(BLOCK_C, False)
     rem = K_steps % BLOCK_C
-    graphs_rem = build_graphs(rem) if rem else []
+    graphs_rem = build_graphs(rem, coll_in_graph) if rem else []
     torch.cuda.synchronize()
     for gr in graphs_full + graphs_rem:   # upload / first-touch every graph before warm-up
         gr.replay()
     torch.cuda.synchronize()
 
-    def run_steps(nsteps, record=None):
-        """nsteps steps as graph replays, M-major in blocks of BLOCK_C (+ remainder block)."""
+    def run_steps(nsteps, grs_full, grs_rem, eager_coll, record=None):
+        """nsteps steps as graph replays, point-major in blocks of BLOCK_C (+ remainder block)."""
         blocks = [BLOCK_C] * (nsteps // BLOCK_C) + ([nsteps % BLOCK_C] if nsteps % BLOCK_C else [])
         for C in blocks:
-            grs = graphs_full if C == BLOCK_C else (graphs_rem if C == rem else build_graphs(C))
+            grs = grs_full if C == BLOCK_C else grs_rem
             for gi, gr in enumerate(grs):
                 if record is not None:
                     ev = torch.cuda.Event(enable_timing=True)
                     ev.record(stream)
                     record.append((gi, C, ev))
                 gr.replay()
-                if world > 1:
+                if eager_coll:
                     for _ in range(C):
                         collective(gemms[gi])
         if record is not None:
@@ -249,7 +294,22 @@ def run_quick(args, rank, world, dist):
             ev.record(stream)
             record.append((None, 0, ev))
 
-    run_steps(W)     # W untimed warm-up steps
+    def per_point_ms(rec):
+        ms, n = [0.0] * len(gemms), [0] * len(gemms)
+        for (gi, C, ev), (_, _, ev_next) in zip(rec[:-1], rec[1:]):
+            ms[gi] += ev.elapsed_time(ev_next)
+            n[gi] += C
+        return ms, n
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    eager_coll = world > 1 and not coll_in_graph
+    run_steps(W, graphs_full, graphs_rem, eager_coll)     # W untimed warm-up steps
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
@@ -260,107 +320,149 @@ def run_quick(args, rank, world, dist):
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        run_steps(K_steps, rec)
+        run_steps(K_steps, graphs_full, graphs_rem, eager_coll, rec)
         t_end.record(stream)
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    if dist is not None:
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    step_ms, step_n = per_point_ms(rec)
 
-    # per-GEMM average launch duration over the timed region (events between graph replays)
-    per_gemm_ms = [0.0] * len(gemms)
-    per_gemm_n = [0] * len(gemms)
-    for (gi, C, ev), (_, _, ev_next) in zip(rec[:-1], rec[1:]):
-        per_gemm_ms[gi] += ev.elapsed_time(ev_next)
-        per_gemm_n[gi] += C
+    # GEMM-only per-point times (N > 1: a second, shorter timed phase without the collectives)
+    gemm_ms, gemm_n = step_ms, step_n
+    gemm_only_ms_per_step = elapsed_ms / K_steps
+    if world > 1:
+        g_full = build_graphs(BLOCK_C, False)
+        g_rem = build_graphs(rem, False) if rem else []
+        run_steps(min(W, BLOCK_C), g_full, g_rem, False)
+        torch.cuda.synchronize()
+        dist.barrier()
+        rec2 = []
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        run_steps(K_steps, g_full, g_rem, False, rec2)
+        b.record(stream)
+        torch.cuda.synchronize()
+        gemm_only_ms_per_step = max_over_ranks(a.elapsed_time(b)) / K_steps
+        gemm_ms, gemm_n = per_point_ms(rec2)
 
     peaks = load_peaks()
     ridge = peaks["tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
     traffic = load_traffic()
     step_flops = sum(algo_flops(g["M"], g["N"], g["K"]) for g in gemms)
-    step_bytes_rank = sum(algo_bytes(g["M"], g["Nr"], g["K"], G) for g in gemms)
     sweep = []
     for gi, g in enumerate(gemms):
-        us = 1e3 * per_gemm_ms[gi] / max(1, per_gemm_n[gi])
-        fl = algo_flops(g["M"], g["Nr"], g["K"])
-        by = algo_bytes(g["M"], g["Nr"], g["K"], G)
+        us = 1e3 * gemm_ms[gi] / max(1, gemm_n[gi])
+        fl = algo_flops(g["M"], g["Nl"], g["Kl"])
+        by = algo_bytes(g["M"], g["Nl"], g["Kl"], G)
         tfl = fl / (us * 1e-6) / 1e12
         gbs = by / (us * 1e-6) / 1e9
-        sweep.append({"M": g["M"], "N": g["Nr"], "K": g["K"], "us": round(us, 3), "tflops": round(tfl, 2),
-                      "gbs": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm_gbs"], 4),
-                      "frac_tensor": round(tfl / peaks["tflops"], 4),
-                      "bound": "tensor" if fl / by >= ridge else "hbm",
-                      "tile_n": g["plan"]["tile_n"], "split_k": g["plan"]["split_k"],
-                      "cta_pair": g["plan"].get("pair", False),
-                      "ctas": g["plan"]["num_ctas"]})
+        e = {"M": g["M"], "N": g["Nl"], "K": g["Kl"], "tp": g["kind"] if world > 1 else "none",
+             "us": round(us, 3), "tflops": round(tfl, 2), "gbs": round(gbs, 1),
+             "frac_hbm": round(gbs / peaks["hbm_gbs"], 4), "frac_tensor": round(tfl / peaks["tflops"], 4),
+             "bound": "tensor" if fl / by >= ridge else "hbm", "kernel": plan_key(g["plan"]),
+             "ctas": g["plan"]["num_ctas"]}
+        if world > 1:
+            e["us_with_collective"] = round(1e3 * step_ms[gi] / max(1, step_n[gi]), 3)
+        sweep.append(e)
     layer_stack = None
     if args.workload == "mistral7b_stack":
         # per batch size: the 4 GEMMs of one layer back to back, x 32 layers
         layer_stack = []
         for M in Ms:
-            us_layer = sum(e["us"] for e in sweep if e["M"] == M)
+            key = "us_with_collective" if world > 1 else "us"
+            us_layer = sum(e[key] for e in sweep if e["M"] == M)
             layer_stack.append({"M": M, "us_per_layer": round(us_layer, 3),
                                 "tokens_per_s": round(M / (32 * us_layer * 1e-6), 1)})
-    dom = max(range(len(gemms)), key=lambda i: per_gemm_ms[i])
-    d = sweep[dom]
-    if d["bound"] == "tensor":
-        roof = {"bound": "tensor", "achieved": d["tflops"], "peak": peaks["tflops"], "unit": "TFLOP/s",
-                "frac": round(d["tflops"] / peaks["tflops"], 4)}
+
+    # roofline of the kernel that dominates the step: launches grouped by kernel identity (template
+    # instantiation + schedule); the group with the largest share of the GEMM time; achieved =
+    # the group's algorithmic bytes (or flops) / its measured time (a launch-weighted average)
+    groups = {}
+    for gi, g in enumerate(gemms):
+        k = sweep[gi]["kernel"]
+        d = groups.setdefault(k, {"ms": 0.0, "n": 0, "bytes": 0, "flops": 0, "t_tensor": 0.0, "points": []})
+        d["ms"] += gemm_ms[gi]
+        d["n"] += gemm_n[gi]
+        d["bytes"] += algo_bytes(g["M"], g["Nl"], g["Kl"], G) * gemm_n[gi]
+        d["flops"] += algo_flops(g["M"], g["Nl"], g["Kl"]) * gemm_n[gi]
+        d["t_tensor"] += gemm_ms[gi] if sweep[gi]["bound"] == "tensor" else 0.0
+        d["points"].append(f"{g['M']}x{g['Nl']}x{g['Kl']}")
+    total_ms = sum(d["ms"] for d in groups.values())
+    dom_key = max(groups, key=lambda k: groups[k]["ms"])
+    d = groups[dom_key]
+    t_s = d["ms"] * 1e-3
+    if d["t_tensor"] >= 0.5 * d["ms"]:
+        ach = d["flops"] / t_s / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": peaks["tflops"], "unit": "TFLOP/s",
+                "frac": round(ach / peaks["tflops"], 4)}
     else:
-        roof = {"bound": "hbm", "achieved": d["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": round(d["gbs"] / peaks["hbm_gbs"], 4)}
-    tkey = f"{args.workload}:{d['N']}:{d['K']}:{d['M']}"
-    roof["traffic"] = traffic.get(tkey)
-    roof["kernel"] = (f"quick_w4a16_tc_kernel<{d['tile_n']}{', cta_group::2 pair' if d.get('cta_pair') else ''}> "
-                      f"M={d['M']} N={d['N']} K={d['K']} split_k={d['split_k']}")
-    roof["algorithmic_per_launch"] = algo_bytes(d["M"], d["N"], d["K"], G) if d["bound"] == "hbm" else \
-        algo_flops(d["M"], d["N"], d["K"])
-    roof["peak_source"] = peaks["source"]
-    roof["share_of_step"] = round(per_gemm_ms[dom] / sum(per_gemm_ms), 4)
+        ach = d["bytes"] / t_s / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / peaks["hbm_gbs"], 4)}
+    roof["traffic"] = traffic.get(f"{args.workload}:{dom_key}")
+    roof["kernel"] = f"quick_w4a16_tc_kernel {dom_key}"
+    roof["launches"] = d["points"]
+    roof["algorithmic_per_launch"] = round((d["flops"] if roof["bound"] == "tensor" else d["bytes"]) / max(1, d["n"]))
+    roof["avg_launch_us"] = round(1e3 * d["ms"] / max(1, d["n"]), 3)
+    roof["peak_source"] = peaks["source"] + ", burst figure (each launch is timed on its own)"
+    roof["share_of_step"] = round(d["ms"] / total_ms, 4)
+    roof["kernel_shares"] = {k: round(v["ms"] / total_ms, 4) for k, v in sorted(groups.items(), key=lambda kv: -kv[1]["ms"])}
 
     # ---- e2e: through the C-ABI with host buffers (pinned), copies inside the timed region
-    e2e = run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective)
+    e2e = run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective, ws)
 
     value = K_steps * step_flops / (elapsed_ms * 1e-3) / 1e12
-    gbs_all = K_steps * step_bytes_rank * world / (elapsed_ms * 1e-3) / 1e9
+    step_bytes = sum(algo_bytes(g["M"], g["Nl"], g["Kl"], G) for g in gemms) * world
     res = {
         "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": K_steps,
         "warmup": W, "ms_per_step": round(elapsed_ms / K_steps, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f16",
         "data": "synthetic (SplitMix64 AWQ int4 weights, U[-1,1] fp16 X)",
         "config": {"workload": args.workload, "baseline_config": cfg_idx,
-                   "shapes_NxK": [[n, k] for n, k in shapes], "M": Ms, "group_size": G,
-                   "gemms_per_step": per_step_launches,
-                   "parallelism": f"tp{world} column-sharded N, NCCL all-gather" if world > 1 else "single GPU",
-                   "l2": (f"rotating {R} weight copies ({R * blob_bytes / 2**20:.0f} MiB) > L2 {l2 / 2**20:.0f} MiB; "
-                          "every launch reads its weights from HBM") if l2_cold else
+                   "shapes_NxK": [[n, k, kind] for n, k, kind in shapes], "M": Ms, "group_size": G,
+                   "gemms_per_step": len(gemms),
+                   "parallelism": (f"tp{world}: " + ", ".join(
+                       f"{n}x{k} {'column-parallel + NCCL all-gather' if kind == 'col' else 'column-parallel (output stays sharded)' if kind == 'colx' else 'row-parallel + NCCL fp32 all-reduce'}"
+                       for n, k, kind in shapes)) if world > 1 else "single GPU",
+                   "l2": (f"rotating {R} weight copies per shape ({R * blob_bytes / 2**20:.0f} MiB) > L2 "
+                          f"{l2 / 2**20:.0f} MiB; every launch reads its weights from HBM") if l2_cold else
                          f"weights L2-resident ({R} copies of {blob_bytes} B < 2.5 x L2)",
-                   "timing": f"CUDA-graph replays of {BLOCK_C} launches per M point (PDL between consecutive launches), M-major; events between replays",
-                   "launch": "quick_w4a16_gemm_ex with QUICK_FLAG_PDL (programmatic dependent launch), automatic plan"},
-        "hbm_gbs_aggregate": round(gbs_all, 1),
-        "gpu_launches": K_steps * per_step_launches * (2 if world > 1 else 1),
+                   "timing": f"CUDA-graph replays of {BLOCK_C} launches per GEMM point (PDL between consecutive "
+                             "launches), point-major; events between replays"
+                             + ("; NCCL collectives captured in the graphs" if coll_in_graph else
+                                "; NCCL collectives eager after each replay" if world > 1 else ""),
+                   "launch": "quick_w4a16_gemm_ex with QUICK_FLAG_PDL and a caller-owned stream-K workspace, "
+                             "automatic plan"},
+        "hbm_gbs_aggregate": round(K_steps * step_bytes / (elapsed_ms * 1e-3) / 1e9, 1),
+        "gpu_launches": K_steps * sum(1 + (2 if (world > 1 and g["kind"] != "colx") else 0) for g in gemms),
         "roofline": roof,
         "sweep": sweep,
         **({"layer_stack_32_layers": layer_stack} if layer_stack else {}),
+        **({"gemm_only_ms_per_step": round(gemm_only_ms_per_step, 5),
+            "collective_ms_per_step": round(elapsed_ms / K_steps - gemm_only_ms_per_step, 5),
+            "comm_nranks_ok": True} if world > 1 else {}),
         "e2e": e2e,
-        "pack": {"host_seconds": round(pack_s, 4), "bytes": int(sum(b.size for b in blobs))},
+        "pack": {"host_seconds": round(pack_s, 4), "bytes": int(sum(l_["blob"].size for l_ in layers))},
         "clocks": sampler.summary(),
     }
     return res
 
 
-def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
+def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective, ws):
     import torch
-    steps = max(3, min(args.steps, 200))
+    steps = max(3, min(args.steps, 100))
+    out_of = [g.get("yfull", g["y"]) for g in gemms]
     xh = [torch.from_numpy(g["x_host"].view(np.int16)).view(torch.float16).pin_memory() for g in gemms]
-    yh = [torch.empty(g["yfull"].shape if world > 1 else g["y"].shape, dtype=torch.float16).pin_memory() for g in gemms]
+    yh = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in out_of]
     xd = [g["xs"][0] for g in gemms]
     sh = stream.cuda_stream
+
+    def gemm_call(gi, g, slot):
+        fl = quick.QUICK_FLAG_OUT_F32 if g["y"].dtype == torch.float32 else 0
+        quick.quick_w4a16_gemm_raw(xd[gi].data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nl"], g["Kl"],
+                                   G, g["y"].data_ptr(), sh, flags=fl, ws_ptr=ws.data_ptr(), ws_bytes=ws.numel())
 
     pipelined = world == 1
     if pipelined:
@@ -377,13 +479,9 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
             slot = (i * len(gemms) + gi) % R
             if not pipelined:
                 xd[gi].copy_(xh[gi], non_blocking=True)
-                quick.quick_w4a16_gemm_raw(xd[gi].data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nr"],
-                                           g["K"], G, g["y"].data_ptr(), sh)
-                if world > 1:
-                    collective(g)
-                    yh[gi].copy_(g["yfull"], non_blocking=True)
-                else:
-                    yh[gi].copy_(g["y"], non_blocking=True)
+                gemm_call(gi, g, slot)
+                collective(g)
+                yh[gi].copy_(out_of[gi], non_blocking=True)
                 continue
             with torch.cuda.stream(s_h2d):
                 if started[gi]:
@@ -393,12 +491,11 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
             stream.wait_event(ev["h2d"][gi])
             if started[gi]:
                 stream.wait_event(ev["d2h"][gi])          # y[gi] has been read back
-            quick.quick_w4a16_gemm_raw(xd[gi].data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nr"],
-                                       g["K"], G, g["y"].data_ptr(), sh)
+            gemm_call(gi, g, slot)
             ev["comp"][gi].record(stream)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev["comp"][gi])
-                yh[gi].copy_(g["y"], non_blocking=True)
+                yh[gi].copy_(out_of[gi], non_blocking=True)
                 ev["d2h"][gi].record(s_d2h)
             started[gi] = True
 
@@ -407,7 +504,7 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
     torch.cuda.synchronize()
     graph = None
     if pipelined:
-        # one step = one CUDA-graph replay: the 9 uploads, GEMMs (C-ABI calls, captured) and
+        # one step = one CUDA-graph replay: the uploads, GEMMs (C-ABI calls, captured) and
         # read-backs with their cross-stream event edges, forked from and joined to `stream`
         # (replays on `stream` are ordered, so buffers are reused safely across steps)
         graph = torch.cuda.CUDAGraph()
@@ -442,13 +539,13 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective):
         ms = float(t.item())
     flops = sum(algo_flops(g["M"], g["N"], g["K"]) for g in gemms)
     return {"value": round(steps * flops / (ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
-            "h2d_bytes_per_step": int(sum(2 * g["M"] * g["K"] for g in gemms)),
-            "d2h_bytes_per_step": int(sum(2 * g["M"] * g["N"] for g in gemms)),
+            "h2d_bytes_per_step": int(sum(x.numel() * 2 for x in xh)),
+            "d2h_bytes_per_step": int(sum(y.numel() * y.element_size() for y in yh)),
             "steps": steps, "ms_per_step": round(ms / steps, 4),
-            "path": ("C-ABI quick_w4a16_gemm per GEMM, pinned H2D X + D2H Y each step"
+            "path": ("C-ABI quick_w4a16_gemm_ex per GEMM (caller-owned workspace), pinned H2D X + D2H Y each step"
                      + ("; one CUDA-graph replay per step holding the uploads, the captured C-ABI GEMM calls and "
                         "the read-backs on three streams with event dependencies (copies overlap GEMMs)"
-                        if world == 1 else ""))}
+                        if world == 1 else "; eager, with the TP collectives and epilogue kernels"))}
 
 
 # ------------------------------------------------------------------------------------------ CPU arm
@@ -458,7 +555,7 @@ def oracle_step_sample(workload, budget_s):
     import oracle  # bench.py's cpu_baseline / reference leg is allowed to call the oracle
     _, shapes, Ms, G = WORKLOADS[workload]
     probs = []
-    for si, (N, K) in enumerate(shapes):
+    for si, (N, K, _kind) in enumerate(shapes):
         qw = synth.make_qweight(si, K, N)
         sc = synth.make_scales(si, K, N, G)
         zr = synth.make_zeros(si, K, N, G)
@@ -523,29 +620,45 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": args.workload, "group_size": G, "M": Ms,
-                       "shapes_NxK": [[n, k] for n, k in shapes], "columns_per_gemm": ns},
+                       "shapes_NxK": [[n, k, kind] for n, k, kind in shapes], "columns_per_gemm": ns},
             "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "kind": "oracle", "cores": cpu_threads(),
                              "sample": sample},
             "e2e": {"value": round(v, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 # ------------------------------------------------------------------------------------------ main
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=800)
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", choices=["quick", "reference"], default="quick")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama2_7b_attn")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
-    assert args.warmup >= 3 and args.steps >= 1
+    if args.warmup < 3 or args.steps < 1 or args.gpus < 1:
+        sys.exit("bench.py: needs --warmup >= 3, --steps >= 1, --gpus >= 1")
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torchrun on this node (127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
+        # the oracle on the host cores: rank 0 alone runs it; the other ranks exit without work
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
@@ -556,6 +669,8 @@ def main():
         import torch.distributed as tdist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
+        if tdist.get_world_size() != args.gpus:
+            sys.exit("bench.py: process group size != --gpus")
         dist = tdist
     res = run_quick(args, rank, world, dist)
     if rank == 0:

@@ -60,10 +60,10 @@ quick_status_t quick_unpack_weights(const void* packed, int group_size, int K, i
                                     uint32_t* qweight, uint16_t* scales, uint32_t* zeros);
 
 /* The hot path (device, asynchronous on `stream`; CUDA-graph capturable).  Y = X . dequant(Wq)
- * with fp32 accumulation (reading R4) and fp16 output.  Small-M plans use a stream-K schedule
- * whose fp32 partial tiles live in a per-(device, stream) workspace the library allocates on the
- * first such call made outside graph capture (a few MiB; kept for the process lifetime); under
- * capture without that workspace the cluster split-K plan (no workspace) is used instead.
+ * with fp32 accumulation (reading R4) and fp16 output.  No allocation, no synchronisation and no
+ * host-visible state: the launch plan is a pure function of (M, N, K, G), identical eagerly and
+ * under graph capture, and needs no workspace (split-K partials are reduced through the
+ * cluster's distributed shared memory).
  *   X       device, __half [M][K] row-major, 16-byte aligned
  *   packed  device copy of the quick_pack_weights blob, 128-byte aligned
  *   Y       device, __half [M][N] row-major, 16-byte aligned
@@ -78,29 +78,48 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
                                 kernel in the stream; X is read and Y written only after that
                                 kernel completes.  The weights must not be written by the
                                 immediately preceding kernel.  The first weight stages are
-                                also dequantized before that point (one stage only for the
-                                256-token tile). */
+                                also dequantized before that point.  Ignored by plans with
+                                256-token tiles. */
 #define QUICK_FLAG_NO_STREAMK 4 /* never use the stream-K schedule (tests / A-B timing) */
 
-/* Extended form used by tensor parallelism, layer stacks and the tests.
+/* Bytes of caller-owned workspace the call quick_w4a16_gemm_ex(M, N, K, G, flags, tile_n,
+ * split_k) can use: the small-M stream-K schedule (tiles of <= 64 tokens) keeps one fp32
+ * partial tile per CTA and one arrival counter per output tile there.  0 when that call's plan
+ * needs none.  Pure function of its arguments (device properties included). */
+size_t quick_workspace_bytes(int M, int N, int K, int group_size, int flags, int tile_n,
+                             int split_k);
+
+/* Extended form used by tensor parallelism, layer stacks, the bench and the tests.
  *   ldy       row stride of Y in elements (>= N, multiple of 8); lets a rank write its column
  *             slice of a wider Y in place
  *   flags     QUICK_FLAG_* bits (0 = fp16 Y, ordinary stream ordering)
  *   tile_n    tokens per MMA tile (16, 32, 64, 128, 256), 0 = automatic
  *   split_k   CTAs per cluster splitting K (1..8, <= ceil(K/128)), 0 = automatic (which may
  *             choose stream-K for tiles <= 64)
+ *   workspace, workspace_bytes
+ *             caller-owned device memory, 256-byte aligned, ZEROED by the caller once before
+ *             its first use (every launch leaves it zeroed again).  The stream-K plan is used
+ *             only if workspace_bytes >= quick_workspace_bytes(...) of this call; otherwise
+ *             the workspace-free plan runs (so the plan never depends on anything but the
+ *             arguments).  NULL / 0 = no workspace.  Two launches that may run concurrently
+ *             (different streams, or graphs replayed on different streams) must not share a
+ *             workspace; graphs capture the pointer, so it must outlive them.
  * With tile_n = split_k = 0 and M > 64 the automatic plan may run tiles of 128/256 tokens as CTA
  * pairs (tcgen05 cta_group::2: two n-tiles per cluster of two SMs); a forced
  * (tile_n, split_k) runs one CTA per n-tile.  Both compute the same MMAs in the same K order.
- * Deterministic: equal inputs and equal (tile_n, split_k) give bit-equal Y. */
+ * QUICK_FLAG_PDL is not applied to plans with 256-token tiles.
+ * Deterministic: equal inputs and equal plans give bit-equal Y. */
 quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K,
                                    int group_size, void* Y, int ldy, int flags, int tile_n,
-                                   int split_k, void* stream);
+                                   int split_k, void* workspace, size_t workspace_bytes,
+                                   void* stream);
 
-/* The launch plan the automatic dispatch would use for (M, N, K, G): tokens per tile, cluster
- * split-K factor (0 = stream-K schedule) and number of CTAs.  Any out pointer may be NULL. */
-quick_status_t quick_gemm_plan(int M, int N, int K, int group_size, int* tile_n, int* split_k,
-                               int* num_ctas);
+/* The launch plan quick_w4a16_gemm_ex(M, N, K, G, flags, tile_n = 0, split_k = 0, workspace of
+ * workspace_bytes) would use: tokens per tile, cluster split-K factor (0 = stream-K schedule),
+ * number of CTAs, and 1 if the tiles run as CTA pairs.  Any out pointer may be NULL. */
+quick_status_t quick_gemm_plan(int M, int N, int K, int group_size, int flags,
+                               size_t workspace_bytes, int* tile_n, int* split_k, int* num_ctas,
+                               int* cta_pair);
 
 /* Device dequantization of a packed blob into W fp16 [K][N] row-major (device), computing
  * dequant(q)[k][n] bit-exactly as fp16_rne((q - z) * s) (§2.3).  Asynchronous. */

@@ -465,11 +465,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       const int k_seg_end = min(sg.a_hi * kKA, K);
       const int nl = (sg.a_hi - sg.a_lo + APL - 1) / APL;
       if (pre < 0) pre = pdl ? (nl < STAGES ? nl : STAGES) : 0;
-      // The 256-token tile prefetches only one stage ahead of X: with its weights for 2-3 load
-      // stages issued before the first X tile, it failed intermittently with "unspecified
-      // launch failure" (tools/pdl_repro.py on B200: pre 3 -> 5 of 6 runs, pre 2 -> 2 of 5,
-      // pre 1 -> 0 of 5; never for tiles <= 128).  Root cause not identified.
-      if (BN == 256 && pre > 1) pre = 1;
+      // (the host never sets QUICK_FLAG_PDL for the 256-token tile)
       for (int l = 0; l < nl; ++l, ++lf) {
         const int kl0 = (sg.a_lo + l * APL) * kKA;
         const int kv = min(C::KL, k_seg_end - kl0);   // valid k in this load stage
@@ -1503,62 +1499,14 @@ int max_resident_pair(int bn, int S) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Stream-K workspace: per (device, stream), allocated on the first call outside graph
-// capture (partial tiles [P][2][BN][128] fp32 + one arrival counter per tile, zeroed once and
-// reset by the kernel).  A call under capture without a large-enough workspace uses the
-// cluster split-K plan instead, which needs none.
-struct Workspace {
-  int dev;
-  cudaStream_t stream;
-  float* ws;
-  size_t ws_bytes;
-  int* sems;
-  size_t n_sems;
-};
-
-bool get_workspace(cudaStream_t stream, size_t ws_bytes, size_t n_sems, float** ws, int** sems) {
-  static std::mutex mu;
-  static std::vector<Workspace> table;
-  const int dev = current_device();
-  std::lock_guard<std::mutex> lock(mu);
-  Workspace* w = nullptr;
-  for (auto& e : table)
-    if (e.dev == dev && e.stream == stream) w = &e;
-  if (w != nullptr && w->ws_bytes >= ws_bytes && w->n_sems >= n_sems) {
-    *ws = w->ws;
-    *sems = w->sems;
-    return true;
-  }
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
-    cudaGetLastError();
-    return false;
-  }
-  const size_t nb = std::max(ws_bytes, w ? w->ws_bytes : (size_t)0);
-  const size_t ns = std::max(n_sems, w ? w->n_sems : (size_t)0);
-  float* new_ws = nullptr;
-  int* new_sems = nullptr;
-  if (cudaMalloc(&new_ws, nb) != cudaSuccess || cudaMalloc(&new_sems, ns * sizeof(int)) != cudaSuccess ||
-      cudaMemsetAsync(new_sems, 0, ns * sizeof(int), stream) != cudaSuccess) {
-    cudaGetLastError();
-    if (new_ws) cudaFree(new_ws);
-    return false;
-  }
-  if (w != nullptr) {
-    // the old buffers may still be used by kernels queued on this stream: free stream-ordered
-    cudaStreamSynchronize(stream);
-    cudaFree(w->ws);
-    cudaFree(w->sems);
-    w->ws = new_ws;
-    w->sems = new_sems;
-    w->ws_bytes = nb;
-    w->n_sems = ns;
-  } else {
-    table.push_back(Workspace{dev, stream, new_ws, nb, new_sems, ns});
-  }
-  *ws = new_ws;
-  *sems = new_sems;
-  return true;
+// Stream-K workspace: CALLER-OWNED (quick_workspace_bytes / the workspace arguments of
+// quick_w4a16_gemm_ex).  Layout: [tiles] int32 arrival counters (zero between launches: the
+// caller zeroes the buffer once, every launch leaves them zero), padded to 256 B, then the
+// [P][BN][128] fp32 partial tiles.  The library never allocates, frees or synchronises.
+constexpr size_t kSemAlign = 256;
+size_t sk_sem_bytes(long long tiles) { return (((size_t)tiles * sizeof(int)) + kSemAlign - 1) / kSemAlign * kSemAlign; }
+size_t sk_ws_bytes(long long tiles, int P, int bn) {
+  return sk_sem_bytes(tiles) + (size_t)P * bn * quick::kTileRows * sizeof(float);
 }
 
 struct Plan {
@@ -1676,6 +1624,19 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
   return Plan{tn, S, tiles * S, false, 0};
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel), not per launch
+cudaError_t set_smem_once(const void* k, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, const void*>> done;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& d : done)
+    if (d.first == dev && d.second == k) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(dev, k);
+  return e;
+}
+
 template <int BN, bool SK>
 quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int P,
                          cudaStream_t stream, bool pair = false) {
@@ -1719,7 +1680,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
                                             : quick::quick_w4a16_tc_kernel<BN, false, false, true, 2>)
                                     : (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, false, 2>
                                             : quick::quick_w4a16_tc_kernel<BN, false, false, false, 2>);
-      e = cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, CP::SMEM_BYTES);
+      e = set_smem_once(reinterpret_cast<const void*>(kq), CP::SMEM_BYTES);
       if (e != cudaSuccess) return cuda_fail(e);
       cfg.gridDim = dim3((unsigned)(2 * S), (unsigned)kp.m_tiles, (unsigned)(kp.n_tiles / 2));
       cfg.dynamicSmemBytes = CP::SMEM_BYTES;
@@ -1746,7 +1707,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
       using CA = quick::Cfg<BN, false, 1>;
       auto* ka = gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, false, 1>
                       : quick::quick_w4a16_tc_kernel<BN, false, false, false, 1>;
-      e = cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, CA::SMEM_BYTES);
+      e = set_smem_once(reinterpret_cast<const void*>(ka), CA::SMEM_BYTES);
       if (e != cudaSuccess) return cuda_fail(e);
       cfg.dynamicSmemBytes = CA::SMEM_BYTES;
       cfg.blockDim = dim3((unsigned)CA::THREADS, 1, 1);
@@ -1763,6 +1724,60 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
              : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, false>, tmap, kp);
   if (e != cudaSuccess) return cuda_fail(e);
   return QUICK_OK;
+}
+
+constexpr int kKnownFlags = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
+                            quick::kDebugExitTop | quick::kDebugExitPrologue | quick::kDebugNoMma |
+                            quick::kDebugOneCta | quick::kDebugNoSttm | quick::kDebugPdlEarly |
+                            quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair | quick::kDebugForceSk;
+
+// The launch plan of a call: a pure function of the shape, flags and overrides, and of whether
+// a stream-K workspace may be used (`allow_ws`).
+Plan plan_for(int M, int N, int K, int G, int flags, int tile_n, int split_k, bool allow_ws) {
+  Plan plan = choose_plan(M, N, K, G, tile_n, split_k,
+                          allow_ws && (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0,
+                          (flags & quick::kDebugNoPair) == 0, (flags & quick::kDebugForceSk) != 0);
+  if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
+  if ((flags & quick::kForcePair) && !plan.sk && plan.tile_n >= 128 && (N / quick::kTileRows) % 2 == 0 &&
+      2 * plan.split <= quick::kMaxSplit)
+    plan.pair = true;
+  return plan;
+}
+
+// TMA descriptor of X viewed as [K/64][M][64], box {64, rows, kc}.  Encoding costs host
+// microseconds, so descriptors are cached per thread, keyed by everything they encode (the
+// pointer, M, K and the box): a hit is always the same descriptor the encoder would produce.
+bool x_tensor_map(const void* X, int M, int K, int rows, int kc, CUtensorMap* out) {
+  struct Entry {
+    const void* x;
+    int M, K, rows, kc;
+    CUtensorMap map;
+  };
+  constexpr int kEntries = 32;
+  thread_local Entry cache[kEntries];
+  thread_local int used = 0, next = 0;
+  for (int i = 0; i < used; ++i) {
+    const Entry& e = cache[i];
+    if (e.x == X && e.M == M && e.K == K && e.rows == rows && e.kc == kc) {
+      *out = e.map;
+      return true;
+    }
+  }
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)rows, (cuuint32_t)kc};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(X), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return false;
+  Entry& e = cache[next];
+  e = Entry{X, M, K, rows, kc, *out};
+  next = (next + 1) % kEntries;
+  if (used < kEntries) ++used;
+  return true;
 }
 
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -1793,81 +1808,72 @@ int quick_debug_resident(int bn, int sk, int S, int* smem_bytes, int* regs) {
   return max_resident(bn, sk != 0, S);
 }
 
-// Debug only: 1 when the automatic plan of this shape uses CTA pairs (cta_group::2)
-int quick_debug_plan_pair(int M, int N, int K, int G) {
-  if (check_gemm_shape(M, N, K, G) != QUICK_OK) return -1;
-  return choose_plan(M > 0 ? M : 1, N, K, G, 0, 0, true).pair ? 1 : 0;
-}
-
-quick_status_t quick_gemm_plan(int M, int N, int K, int G, int* tile_n, int* split_k,
-                               int* num_ctas) {
+quick_status_t quick_gemm_plan(int M, int N, int K, int G, int flags, size_t workspace_bytes, int* tile_n,
+                               int* split_k, int* num_ctas, int* cta_pair) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
-  const Plan p = choose_plan(M > 0 ? M : 1, N, K, G, 0, 0, true);
+  if ((flags & ~kKnownFlags) != 0) return QUICK_ERR_UNSUPPORTED;
+  const int Mp = M > 0 ? M : 1;
+  Plan p = plan_for(Mp, N, K, G, flags, 0, 0, true);
+  if (p.sk) {
+    const long long tiles = (long long)(N / quick::kTileRows) * ((Mp + p.tile_n - 1) / p.tile_n);
+    if (workspace_bytes < sk_ws_bytes(tiles, p.P, p.tile_n)) p = plan_for(Mp, N, K, G, flags, 0, 0, false);
+  }
   if (tile_n) *tile_n = p.tile_n;
   if (split_k) *split_k = p.sk ? 0 : p.split;   // 0 = stream-K
   if (num_ctas) *num_ctas = p.ctas;
+  if (cta_pair) *cta_pair = p.pair ? 1 : 0;
   return QUICK_OK;
+}
+
+size_t quick_workspace_bytes(int M, int N, int K, int G, int flags, int tile_n, int split_k) {
+  if (check_gemm_shape(M, N, K, G) != QUICK_OK || M == 0) return 0;
+  if (tile_n != 0 && tile_index(tile_n) < 0) return 0;
+  const Plan plan = plan_for(M, N, K, G, flags, tile_n, split_k, true);
+  if (!plan.sk) return 0;
+  const long long tiles = (long long)(N / quick::kTileRows) * ((M + plan.tile_n - 1) / plan.tile_n);
+  return sk_ws_bytes(tiles, plan.P, plan.tile_n);
 }
 
 quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K, int G,
                                    void* Y, int ldy, int flags, int tile_n, int split_k,
-                                   void* stream) {
+                                   void* workspace, size_t workspace_bytes, void* stream) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
   if (M == 0) return QUICK_OK;
   if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
   if (ldy < N) return QUICK_ERR_INVALID_ARG;
-  const int known = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
-                    quick::kDebugExitTop | quick::kDebugExitPrologue |
-                    quick::kDebugNoMma | quick::kDebugOneCta | quick::kDebugNoSttm |
-                    quick::kDebugPdlEarly | quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair |
-                    quick::kDebugForceSk;
-  if (ldy % 8 != 0 || (flags & ~known) != 0) return QUICK_ERR_UNSUPPORTED;
+  if (ldy % 8 != 0 || (flags & ~kKnownFlags) != 0) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
+  if (workspace_bytes != 0 && (workspace == nullptr || !aligned(workspace, 256))) return QUICK_ERR_INVALID_ARG;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   if (split_k < 0 || split_k > quick::kMaxSplit || split_k > NA) return QUICK_ERR_UNSUPPORTED;
 
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
-  Plan plan = choose_plan(M, N, K, G, tile_n, split_k,
-                          (flags & (QUICK_FLAG_NO_STREAMK | quick::kAblationSmemA)) == 0,
-                          (flags & quick::kDebugNoPair) == 0, (flags & quick::kDebugForceSk) != 0);
-  if ((flags & quick::kDebugOneCta) && plan.sk) plan.P = plan.ctas = std::min(plan.P, sm_count());
-  if ((flags & quick::kForcePair) && !plan.sk && plan.tile_n >= 128 && (N / quick::kTileRows) % 2 == 0 &&
-      2 * plan.split <= quick::kMaxSplit)
-    plan.pair = true;
+  // The plan is a pure function of the arguments: stream-K only when the caller's workspace
+  // holds it (never a hidden allocation; the same plan eager and under graph capture).
+  Plan plan = plan_for(M, N, K, G, flags, tile_n, split_k, true);
   quick::KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.n_tiles = N / quick::kTileRows;
-  kp.m_tiles = (M + plan.tile_n - 1) / plan.tile_n;
   if (plan.sk) {
-    float* ws = nullptr;
-    int* sems = nullptr;
-    const size_t ws_bytes = (size_t)plan.P * plan.tile_n * quick::kTileRows * sizeof(float);
-    if (get_workspace(strm, ws_bytes, (size_t)kp.n_tiles * kp.m_tiles, &ws, &sems)) {
-      kp.ws = ws;
-      kp.sems = sems;
+    const long long tiles = (long long)kp.n_tiles * ((M + plan.tile_n - 1) / plan.tile_n);
+    if (workspace_bytes >= sk_ws_bytes(tiles, plan.P, plan.tile_n)) {
+      kp.sems = static_cast<int*>(workspace);
+      kp.ws = reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + sk_sem_bytes(tiles));
     } else {
-      plan = choose_plan(M, N, K, G, tile_n, split_k, false);   // no workspace (graph capture)
+      plan = plan_for(M, N, K, G, flags, tile_n, split_k, false);
     }
   }
+  kp.m_tiles = (M + plan.tile_n - 1) / plan.tile_n;
   const int tn = plan.tile_n, s = plan.split;
 
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return cuda_fail(cudaErrorInitializationError);
   // X viewed as [K/64][M][64] (dims innermost first: k within a 64-chunk, token, k-chunk): one
   // 3-D box {64, tile_n, KL/64} lands as KL/64 SWIZZLE_128B [tile_n][64] sub-tiles.
   CUtensorMap tmap;
   const int kl = kl_for(tn, plan.sk);
-  cuuint64_t dims[3] = {64, (cuuint64_t)M, (cuuint64_t)(K / 64)};
-  cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
-  cuuint32_t box[3] = {64, (cuuint32_t)(plan.pair ? tn / 2 : tn), (cuuint32_t)(kl / 64)};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(X), dims, strides,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
+  if (!x_tensor_map(X, M, K, plan.pair ? tn / 2 : tn, kl / 64, &tmap)) return cuda_fail(cudaErrorInvalidValue);
 
   kp.packed = static_cast<const uint8_t*>(packed);
   kp.Y = Y;
@@ -1881,7 +1887,9 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
     while ((1 << kp.g_shift) < G) ++kp.g_shift;
   }
   kp.ldy = ldy;
-  kp.flags = flags;
+  // the 256-token tile launches without programmatic dependent launch (an
+  // intermittent fault with deeper PDL prefetch whose root cause is not established)
+  kp.flags = (tn == 256) ? (flags & ~QUICK_FLAG_PDL) : flags;
   kp.NA = NA;
   kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;
@@ -1905,7 +1913,7 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
 
 quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N, int K, int G,
                                 void* Y, void* stream) {
-  return quick_w4a16_gemm_ex(X, packed, M, N, K, G, Y, N, 0, 0, 0, stream);
+  return quick_w4a16_gemm_ex(X, packed, M, N, K, G, Y, N, 0, 0, 0, nullptr, 0, stream);
 }
 
 quick_status_t quick_dequant_weights(const void* packed, int K, int N, int G, void* W,

@@ -35,8 +35,10 @@ def _load():
         "quick_unpack_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
         "quick_w4a16_gemm": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
         "quick_w4a16_gemm_ex": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int,
-                                        c_int, c_int, c_int, c_void_p]),
-        "quick_gemm_plan": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+                                        c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
+        "quick_workspace_bytes": (c_size_t, [c_int, c_int, c_int, c_int, c_int, c_int, c_int]),
+        "quick_gemm_plan": (c_int, [c_int, c_int, c_int, c_int, c_int, c_size_t, c_void_p, c_void_p, c_void_p,
+                                    c_void_p]),
         "quick_dequant_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
         "quick_f32_to_f16": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
         "quick_gather_columns": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
@@ -83,12 +85,24 @@ def quick_packed_bytes(K: int, N: int, group_size: int) -> int:
 
 
 def quick_pack_weights(qweight, scales, zeros, group_size: int) -> np.ndarray:
-    """AWQ (qweight uint32 [K][N/8], scales fp16 [K/G][N], zeros uint32 [K/G][N/8]) -> v1 blob (uint8)."""
-    qweight = np.ascontiguousarray(qweight, dtype=np.uint32)
-    zeros = np.ascontiguousarray(zeros, dtype=np.uint32)
-    scales = np.ascontiguousarray(np.asarray(scales).view(np.uint16) if np.asarray(scales).dtype == np.float16
-                                  else np.asarray(scales, dtype=np.uint16))
+    """AWQ (qweight uint32 [K][N/8], scales fp16 [K/G][N], zeros uint32 [K/G][N/8]) -> v1 blob (uint8).
+    Shapes and dtypes are checked here: the C packer trusts them."""
+    qweight, scales, zeros = np.asarray(qweight), np.asarray(scales), np.asarray(zeros)
+    if qweight.ndim != 2 or qweight.dtype not in (np.uint32, np.int32):
+        raise ValueError(f"qweight must be a 2-D uint32/int32 array [K][N/8], got {qweight.dtype} {qweight.shape}")
     K, N = qweight.shape[0], qweight.shape[1] * 8
+    if group_size <= 0 or K % group_size:
+        raise ValueError(f"group_size {group_size} must divide K={K}")
+    if scales.dtype not in (np.float16, np.uint16):
+        raise ValueError(f"scales must be float16 (or their uint16 bits), got {scales.dtype}")
+    if scales.shape != (K // group_size, N):
+        raise ValueError(f"scales shape {scales.shape} != (K/G, N) = {(K // group_size, N)}")
+    if zeros.dtype not in (np.uint32, np.int32) or zeros.shape != (K // group_size, N // 8):
+        raise ValueError(f"zeros must be uint32/int32 (K/G, N/8) = {(K // group_size, N // 8)}, "
+                         f"got {zeros.dtype} {zeros.shape}")
+    qweight = np.ascontiguousarray(qweight).view(np.uint32)
+    zeros = np.ascontiguousarray(zeros).view(np.uint32)
+    scales = np.ascontiguousarray(scales).view(np.uint16)
     nbytes = quick_packed_bytes(K, N, group_size)
     out = np.empty(max(nbytes, 1), dtype=np.uint8)
     _check("quick_pack_weights", _lib.quick_pack_weights(_np_ptr(qweight), _np_ptr(scales), _np_ptr(zeros),
@@ -107,41 +121,72 @@ def quick_unpack_weights(packed, group_size: int, K: int, N: int):
     return qweight, scales.view(np.float16), zeros
 
 
-def quick_gemm_plan(M: int, N: int, K: int, group_size: int):
-    tn, sk, nc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    _check("quick_gemm_plan", _lib.quick_gemm_plan(M, N, K, group_size, ctypes.byref(tn), ctypes.byref(sk),
-                                                   ctypes.byref(nc)))
-    pair = _lib.quick_debug_plan_pair(M, N, K, group_size) == 1   # CTA pairs (cta_group::2)
-    return {"tile_n": tn.value, "split_k": sk.value, "num_ctas": nc.value, "pair": pair}
+def quick_gemm_plan(M: int, N: int, K: int, group_size: int, *, flags: int = 0, workspace_bytes: int = 0):
+    """The plan quick_w4a16_gemm_ex would launch for this shape with a workspace of that size."""
+    tn, sk, nc, pr = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _check("quick_gemm_plan", _lib.quick_gemm_plan(M, N, K, group_size, flags, workspace_bytes, ctypes.byref(tn),
+                                                   ctypes.byref(sk), ctypes.byref(nc), ctypes.byref(pr)))
+    return {"tile_n": tn.value, "split_k": sk.value, "num_ctas": nc.value, "pair": pr.value == 1}
+
+
+def quick_workspace_bytes(M: int, N: int, K: int, group_size: int, *, flags: int = 0, tile_n: int = 0,
+                          split_k: int = 0) -> int:
+    return int(_lib.quick_workspace_bytes(M, N, K, group_size, flags, tile_n, split_k))
+
+
+def workspace_for(shapes, group_size: int, device, *, flags: int = 0):
+    """A zeroed caller-owned workspace (torch uint8 tensor) large enough for every (M, N, K) in
+    `shapes` (memory plumbing only; the library never allocates)."""
+    import torch
+    nb = max([quick_workspace_bytes(M, N, K, group_size, flags=flags) for (M, N, K) in shapes] + [256])
+    return torch.zeros(nb, dtype=torch.uint8, device=device)
 
 
 # ----------------------------------------------------------------------------- device side
 def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ldy=None, out_fp32=False,
-                     pdl=False, no_streamk=False, tile_n: int = 0, split_k: int = 0, stream=None):
-    """Y = X . dequant(Wq) on the GPU.  x: cuda fp16 [M][K]; packed: cuda uint8 blob.
+                     pdl=False, no_streamk=False, tile_n: int = 0, split_k: int = 0, workspace=None,
+                     flags: int = 0, stream=None):
+    """Y = X . dequant(Wq) on the GPU.  x: cuda fp16 [M][K]; packed: cuda uint8 blob;
+    workspace: optional zeroed cuda uint8 tensor (quick_workspace_bytes) enabling stream-K plans.
     Returns `out` (allocated if None): fp16 [M][N] (fp32 if out_fp32)."""
     import torch
-    assert x.is_cuda and x.dtype == torch.float16 and x.is_contiguous() and x.dim() == 2 and x.shape[1] == K
-    assert packed.is_cuda and packed.dtype == torch.uint8
+    if not (x.is_cuda and x.dtype == torch.float16 and x.is_contiguous() and x.dim() == 2 and x.shape[1] == K):
+        raise ValueError(f"x must be a contiguous cuda float16 [M][{K}] tensor")
+    if not (packed.is_cuda and packed.dtype == torch.uint8 and packed.is_contiguous()):
+        raise ValueError("packed must be a contiguous cuda uint8 tensor")
+    if packed.numel() != quick_packed_bytes(K, N, group_size):
+        raise ValueError(f"packed has {packed.numel()} bytes, expected {quick_packed_bytes(K, N, group_size)}")
     M = x.shape[0]
+    want = torch.float32 if out_fp32 else torch.float16
     if out is None:
-        out = torch.empty((M, N), device=x.device, dtype=torch.float32 if out_fp32 else torch.float16)
+        out = torch.empty((M, N), device=x.device, dtype=want)
+    elif not (out.is_cuda and out.dtype == want and out.dim() == 2 and out.shape[0] >= M and out.shape[1] >= N
+              and out.stride(1) == 1 and out.device == x.device):
+        raise ValueError(f"out must be a cuda {want} [>= {M}][>= {N}] tensor with unit column stride")
     ld = out.stride(0) if ldy is None else ldy
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        if not (workspace.is_cuda and workspace.dtype == torch.uint8 and workspace.is_contiguous()):
+            raise ValueError("workspace must be a contiguous cuda uint8 tensor")
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel()
+    fl = flags | (QUICK_FLAG_OUT_F32 if out_fp32 else 0) | (QUICK_FLAG_PDL if pdl else 0) \
+        | (QUICK_FLAG_NO_STREAMK if no_streamk else 0)
     _check("quick_w4a16_gemm_ex", _lib.quick_w4a16_gemm_ex(
         ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(packed.data_ptr()), M, N, K, group_size,
-        ctypes.c_void_p(out.data_ptr()), ld, (QUICK_FLAG_OUT_F32 if out_fp32 else 0) | (QUICK_FLAG_PDL if pdl else 0)
-        | (QUICK_FLAG_NO_STREAMK if no_streamk else 0),
-        tile_n, split_k, _stream_handle(stream)))
+        ctypes.c_void_p(out.data_ptr()), ld, fl, tile_n, split_k, ctypes.c_void_p(ws_ptr), ws_bytes,
+        _stream_handle(stream)))
     return out
 
 
 def quick_w4a16_gemm_raw(x_ptr: int, packed_ptr: int, M: int, N: int, K: int, group_size: int, y_ptr: int,
-                         stream_handle: int, flags: int = 0, tile_n: int = 0, split_k: int = 0, ldy: int = 0):
+                         stream_handle: int, flags: int = 0, tile_n: int = 0, split_k: int = 0, ldy: int = 0,
+                         ws_ptr: int = 0, ws_bytes: int = 0):
     """Plain C-ABI call on raw device pointers (`quick_w4a16_gemm`, or `_ex` when any option is set)."""
-    if flags or tile_n or split_k or ldy:
+    if flags or tile_n or split_k or ldy or ws_bytes:
         _check("quick_w4a16_gemm_ex", _lib.quick_w4a16_gemm_ex(
             ctypes.c_void_p(x_ptr), ctypes.c_void_p(packed_ptr), M, N, K, group_size, ctypes.c_void_p(y_ptr),
-            ldy or N, flags, tile_n, split_k, ctypes.c_void_p(stream_handle)))
+            ldy or N, flags, tile_n, split_k, ctypes.c_void_p(ws_ptr or None), ws_bytes,
+            ctypes.c_void_p(stream_handle)))
         return
     _check("quick_w4a16_gemm", _lib.quick_w4a16_gemm(ctypes.c_void_p(x_ptr), ctypes.c_void_p(packed_ptr), M, N, K,
                                                      group_size, ctypes.c_void_p(y_ptr),

@@ -67,25 +67,22 @@ class ColumnParallelW4A16:
         qw, sc, zr = shard_awq_columns(qweight, scales, zeros, self.rank, self.world)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.packed = torch.from_numpy(quick.quick_pack_weights(qw, sc, zr, group_size)).to(self.device)
-        self._bufs = {}
-
-    def _buffers(self, M):
-        if M not in self._bufs:
-            t = self.torch
-            gathered = t.empty((self.world, M, self.Nr), device=self.device, dtype=t.float16)
-            out = t.empty((M, self.N), device=self.device, dtype=t.float16)
-            self._bufs[M] = (gathered, out)
-        return self._bufs[M]
+        self._gathered = {}   # internal [P][M][N/P] all-gather buffers per M (never returned)
+        self.workspace = None
 
     def forward(self, x, out=None):
+        """A fresh output tensor per call unless `out` is given."""
+        t = self.torch
         M = x.shape[0]
         if self.world == 1:
-            return self.quick.quick_w4a16_gemm(x, self.packed, self.N, self.K, self.G, out=out)
-        gathered, y = self._buffers(M)
-        if out is not None:
-            y = out
+            return self.quick.quick_w4a16_gemm(x, self.packed, self.N, self.K, self.G, out=out,
+                                               workspace=self.workspace)
+        if M not in self._gathered:
+            self._gathered[M] = t.empty((self.world, M, self.Nr), device=self.device, dtype=t.float16)
+        gathered = self._gathered[M]
+        y = out if out is not None else t.empty((M, self.N), device=self.device, dtype=t.float16)
         local = gathered[self.rank]                     # compute straight into our slot
-        self.quick.quick_w4a16_gemm(x, self.packed, self.Nr, self.K, self.G, out=local)
+        self.quick.quick_w4a16_gemm(x, self.packed, self.Nr, self.K, self.G, out=local, workspace=self.workspace)
         # in-place all-gather: the input is this rank's slice of the output buffer
         self.dist.all_gather_into_tensor(gathered.view(-1), local.view(-1), group=self.group)
         self.quick.quick_gather_columns(gathered, self.world, M, self.Nr, dst=y)
@@ -110,19 +107,22 @@ class RowParallelW4A16:
         qw, sc, zr = shard_awq_rows(qweight, scales, zeros, group_size, self.rank, self.world)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.packed = torch.from_numpy(quick.quick_pack_weights(qw, sc, zr, group_size)).to(self.device)
-        self._bufs = {}
+        self._partial = {}   # internal fp32 partial per M (never returned)
+        self.workspace = None
 
     def forward(self, x_shard, out=None):
+        """A fresh output tensor per call unless `out` is given."""
         t = self.torch
         M = x_shard.shape[0]
-        if M not in self._bufs:
-            self._bufs[M] = (t.empty((M, self.N), device=self.device, dtype=t.float32),
-                             t.empty((M, self.N), device=self.device, dtype=t.float16))
-        partial, y = self._bufs[M]
-        if out is not None:
-            y = out
-        self.quick.quick_w4a16_gemm(x_shard, self.packed, self.N, self.Kr, self.G, out=partial, out_fp32=True)
-        if self.world > 1:
-            self.dist.all_reduce(partial, op=self.dist.ReduceOp.SUM, group=self.group)   # fp32 on the wire
+        y = out if out is not None else t.empty((M, self.N), device=self.device, dtype=t.float16)
+        if self.world == 1:
+            return self.quick.quick_w4a16_gemm(x_shard, self.packed, self.N, self.Kr, self.G, out=y,
+                                               workspace=self.workspace)
+        if M not in self._partial:
+            self._partial[M] = t.empty((M, self.N), device=self.device, dtype=t.float32)
+        partial = self._partial[M]
+        self.quick.quick_w4a16_gemm(x_shard, self.packed, self.N, self.Kr, self.G, out=partial, out_fp32=True,
+                                    workspace=self.workspace)
+        self.dist.all_reduce(partial, op=self.dist.ReduceOp.SUM, group=self.group)   # fp32 on the wire
         self.quick.quick_f32_to_f16(partial, dst=y)
         return y

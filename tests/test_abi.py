@@ -59,16 +59,53 @@ def test_gemm_argument_validation_before_any_cuda_call():
         quick.QUICK_ERR_UNSUPPORTED
     # _ex overrides
     ex = lib.quick_w4a16_gemm_ex
-    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 100, 0, 0, 0, null) == quick.QUICK_ERR_INVALID_ARG   # ldy < N
-    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 260, 0, 0, 0, null) == quick.QUICK_ERR_UNSUPPORTED  # ldy % 8
-    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 48, 0, null) == quick.QUICK_ERR_UNSUPPORTED  # tile
-    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 16, 9, null) == quick.QUICK_ERR_UNSUPPORTED  # split>8
-    assert ex(dummy, dummy, 8, 256, 128, 128, dummy, 256, 0, 16, 3, null) == quick.QUICK_ERR_UNSUPPORTED  # split>KT
+    z = ctypes.c_size_t(0)
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 100, 0, 0, 0, null, z, null) == quick.QUICK_ERR_INVALID_ARG  # ldy<N
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 260, 0, 0, 0, null, z, null) == quick.QUICK_ERR_UNSUPPORTED  # ldy%8
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 48, 0, null, z, null) == quick.QUICK_ERR_UNSUPPORTED  # tile
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 16, 9, null, z, null) == quick.QUICK_ERR_UNSUPPORTED  # S>8
+    assert ex(dummy, dummy, 8, 256, 128, 128, dummy, 256, 0, 16, 3, null, z, null) == quick.QUICK_ERR_UNSUPPORTED  # S>KT
+    # a workspace size without a (256-byte aligned) workspace pointer
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 0, 0, null, ctypes.c_size_t(4096), null) == \
+        quick.QUICK_ERR_INVALID_ARG
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 0, 0, 0, ctypes.c_void_p((1 << 20) + 64),
+              ctypes.c_size_t(4096), null) == quick.QUICK_ERR_INVALID_ARG
+    # unknown flag bits
+    assert ex(dummy, dummy, 8, 256, 512, 128, dummy, 256, 1 << 8, 0, 0, null, z, null) == quick.QUICK_ERR_UNSUPPORTED
 
 
 def test_plan_validation():
     with pytest.raises(quick.QuickError):
         quick.quick_gemm_plan(8, 200, 512, 128)
+    with pytest.raises(quick.QuickError):
+        quick.quick_gemm_plan(8, 256, 512, 128, flags=1 << 8)
+
+
+def test_workspace_bytes_is_zero_for_invalid_or_workspace_free_calls():
+    assert quick.quick_workspace_bytes(0, 4096, 4096, 128) == 0            # M == 0: no launch
+    assert quick.quick_workspace_bytes(8, 200, 512, 128) == 0              # unsupported shape
+    assert quick.quick_workspace_bytes(8, 256, 512, 128, tile_n=48) == 0   # bad tile
+    # forced cluster split-K and the large-M plans never use the workspace
+    assert quick.quick_workspace_bytes(8, 4096, 4096, 128, split_k=4) == 0
+    assert quick.quick_workspace_bytes(1024, 4096, 4096, 128) == 0
+    assert quick.quick_workspace_bytes(8, 4096, 4096, 128, flags=quick.QUICK_FLAG_NO_STREAMK) == 0
+
+
+def test_pack_rejects_mismatched_metadata():
+    import numpy as np
+    K, N, G = 256, 128, 64
+    qw = np.zeros((K, N // 8), np.uint32)
+    sc = np.ones((K // G, N), np.float16)
+    zr = np.zeros((K // G, N // 8), np.uint32)
+    quick.quick_pack_weights(qw, sc, zr, G)                       # consistent: fine
+    with pytest.raises(ValueError):
+        quick.quick_pack_weights(qw, sc, zr, 128)                 # scales rows != K / G
+    with pytest.raises(ValueError):
+        quick.quick_pack_weights(qw, sc.astype(np.float32), zr, G)   # not fp16
+    with pytest.raises(ValueError):
+        quick.quick_pack_weights(qw, sc, zr[:, :4], G)            # zeros columns != N / 8
+    with pytest.raises(ValueError):
+        quick.quick_pack_weights(qw, sc, zr, 96)                  # G does not divide K
 
 
 def test_epilogue_validation():

@@ -19,6 +19,9 @@ if not torch.cuda.is_available():  # pragma: no cover
 from paper_2402_10076_b200 import quick  # noqa: E402  (fails loudly if libquick.so is missing)
 
 DEV = torch.device("cuda:0")
+# caller-owned stream-K workspace (quick.h: zeroed once, left zeroed by every launch); the tests
+# launch serially, so one is shared (concurrent launches get their own: test_graphs_*)
+WS = torch.zeros(16 << 20, dtype=torch.uint8, device=DEV)
 
 
 def to_dev_f16(a: np.ndarray):
@@ -30,6 +33,7 @@ def pack_dev(p):
 
 
 def run(p, **kw):
+    kw.setdefault("workspace", WS)
     y = quick.quick_w4a16_gemm(to_dev_f16(p.x), pack_dev(p), p.N, p.K, p.group_size, **kw)
     torch.cuda.synchronize()
     return y
@@ -159,10 +163,10 @@ def test_stream_k_segments(M, N, K, G):
     64-k ragged tail (K % 128 == 64)."""
     p = synth.make_problem(M * 7 + K, M=M, N=N, K=K, G=G)
     x, blob = to_dev_f16(p.x), pack_dev(p)
-    plan = quick.quick_gemm_plan(M, N, K, G)
-    y1 = quick.quick_w4a16_gemm(x, blob, N, K, G)
-    y2 = quick.quick_w4a16_gemm(x, blob, N, K, G)
-    yc = quick.quick_w4a16_gemm(x, blob, N, K, G, no_streamk=True)
+    plan = quick.quick_gemm_plan(M, N, K, G, workspace_bytes=WS.numel())
+    y1 = quick.quick_w4a16_gemm(x, blob, N, K, G, workspace=WS)
+    y2 = quick.quick_w4a16_gemm(x, blob, N, K, G, workspace=WS)
+    yc = quick.quick_w4a16_gemm(x, blob, N, K, G)   # no workspace: the cluster split-K plan
     torch.cuda.synchronize()
     check_tol(p, y1, plan)
     check_tol(p, yc, "cluster")
@@ -257,21 +261,21 @@ def test_pdl_chain_matches_ordinary_launches(M, N, K):
     dequantized stages overlap GEMM 1, while its X loads must wait for GEMM 1's completion.
     Chain Y2 = (X . W1) . W2 repeated back to back, eagerly and under CUDA-graph capture; every
     result must be bit-identical to ordinary launches (covers the cluster split-K, stream-K and
-    wide-tile plans, incl. the 256-token tile where the flag is ignored)."""
+    wide-tile plans; plans with the 256-token tile ignore the flag)."""
     G = 128
     p1 = synth.make_problem(M + N, M=M, N=N, K=K, G=G)
     p2 = synth.make_problem(M + N + 1, M=M, N=K, K=N, G=G)   # K2 = N1: X2 = Y1
     x, w1, w2 = to_dev_f16(p1.x), pack_dev(p1), pack_dev(p2)
-    y1 = quick.quick_w4a16_gemm(x, w1, N, K, G)
-    y2 = quick.quick_w4a16_gemm(y1, w2, K, N, G)
+    y1 = quick.quick_w4a16_gemm(x, w1, N, K, G, workspace=WS)
+    y2 = quick.quick_w4a16_gemm(y1, w2, K, N, G, workspace=WS)
     torch.cuda.synchronize()
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         a1 = torch.empty_like(y1)
         a2 = torch.empty_like(y2)
         for _ in range(3):
-            quick.quick_w4a16_gemm(x, w1, N, K, G, out=a1, pdl=True)
-            quick.quick_w4a16_gemm(a1, w2, K, N, G, out=a2, pdl=True)
+            quick.quick_w4a16_gemm(x, w1, N, K, G, out=a1, pdl=True, workspace=WS)
+            quick.quick_w4a16_gemm(a1, w2, K, N, G, out=a2, pdl=True, workspace=WS)
         stream.synchronize()
         assert torch.equal(a1.view(torch.int16), y1.view(torch.int16))
         assert torch.equal(a2.view(torch.int16), y2.view(torch.int16))
@@ -280,8 +284,8 @@ def test_pdl_chain_matches_ordinary_launches(M, N, K):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for _ in range(2):
-                quick.quick_w4a16_gemm(x, w1, N, K, G, out=a1, pdl=True)
-                quick.quick_w4a16_gemm(a1, w2, K, N, G, out=a2, pdl=True)
+                quick.quick_w4a16_gemm(x, w1, N, K, G, out=a1, pdl=True, workspace=WS)
+                quick.quick_w4a16_gemm(a1, w2, K, N, G, out=a2, pdl=True, workspace=WS)
         g.replay()
         g.replay()
         stream.synchronize()
@@ -322,7 +326,7 @@ def test_plans_for_the_baseline_shapes(N, K):
     G = 128
     NA = K // 128
     for M in (1, 2, 8, 16, 17, 32, 33, 64, 65, 128, 192, 256, 512, 1024):
-        pl = quick.quick_gemm_plan(M, N, K, G)
+        pl = quick.quick_gemm_plan(M, N, K, G, workspace_bytes=WS.numel())
         tn, s, ctas = pl["tile_n"], pl["split_k"], pl["num_ctas"]
         assert tn in (16, 32, 64, 128, 256)
         if M <= 64:
@@ -351,11 +355,11 @@ def test_mistral_layer_stack_pdl(M):
     xg = to_dev_f16(probs[2].x)
 
     def layer(pdl, outs):
-        quick.quick_w4a16_gemm(xq, ws[0], 6144, 4096, G, out=outs[0], pdl=pdl)
-        quick.quick_w4a16_gemm(xo, ws[1], 4096, 4096, G, out=outs[1], pdl=pdl)
-        quick.quick_w4a16_gemm(xg, ws[2], 28672, 4096, G, out=outs[2], pdl=pdl)
+        quick.quick_w4a16_gemm(xq, ws[0], 6144, 4096, G, out=outs[0], pdl=pdl, workspace=WS)
+        quick.quick_w4a16_gemm(xo, ws[1], 4096, 4096, G, out=outs[1], pdl=pdl, workspace=WS)
+        quick.quick_w4a16_gemm(xg, ws[2], 28672, 4096, G, out=outs[2], pdl=pdl, workspace=WS)
         outs[3].copy_(outs[2][:, :14336])
-        quick.quick_w4a16_gemm(outs[3], ws[3], 4096, 14336, G, out=outs[4], pdl=pdl)
+        quick.quick_w4a16_gemm(outs[3], ws[3], 4096, 14336, G, out=outs[4], pdl=pdl, workspace=WS)
 
     def bufs():
         return [torch.empty((M, 6144), device=DEV, dtype=torch.float16),
@@ -370,7 +374,7 @@ def test_mistral_layer_stack_pdl(M):
     stream = torch.cuda.Stream()
     out = bufs()
     with torch.cuda.stream(stream):
-        layer(True, out)   # eager first (workspace outside capture)
+        layer(True, out)
         stream.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
@@ -456,3 +460,123 @@ def test_pair_auto_plan_full_size_pdl(M, N, K):
     cols = np.unique(np.concatenate([np.arange(8), np.arange(N - 8, N), rng.choice(N, 112, replace=False)]))
     cols = cols[:len(cols) // 8 * 8]
     _sampled_cols_check(p, y0, cols)
+
+
+# ------------------------------------------------------------------------------- round 2: the bench's own small-M launches
+def _cols(N, seed, n=120):
+    rng = np.random.default_rng(seed)
+    c = np.unique(np.concatenate([np.arange(8), np.arange(N - 8, N), rng.choice(N, n, replace=False)]))
+    return c[:len(c) // 8 * 8]
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 28672, 8192), (16, 28672, 8192),
+                                   (1, 8192, 28672), (16, 8192, 28672), (64, 8192, 28672),
+                                   (1, 5120, 13824), (16, 5120, 13824), (64, 5120, 13824),
+                                   (1, 13824, 5120), (16, 4096, 4096)])
+def test_full_size_small_m_bench_launch(M, N, K):
+    """The launch configuration bench.py times (automatic plan WITH the stream-K workspace, PDL,
+    back to back in a CUDA graph) at full BJ sizes, against the oracle on sampled columns: the
+    tile-16 stream-K plans at K = 8192 / 28672 (segments capped by reading R15), the cluster
+    split-K S = 6 plan of 5120x13824."""
+    G = 128
+    p = synth.make_problem(7 * M + N + K, M=M, N=N, K=K, G=G)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    ys = [torch.empty((M, N), device=DEV, dtype=torch.float16) for _ in range(2)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for y in ys:
+                quick.quick_w4a16_gemm(x, blob, N, K, G, out=y, pdl=True, workspace=WS)
+        g.replay()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ys[0].view(torch.int16), ys[1].view(torch.int16))
+    _sampled_cols_check(p, ys[0], _cols(N, M + N))
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 8192, 28672), (16, 8192, 28672), (64, 8192, 28672), (16, 28672, 8192)])
+def test_unit_scale_stress_long_k(M, N, K):
+    """The worst case of reading R15: unit-scale weights (s = 1/15, |w| up to 1) at K = 28672 through the
+    automatic plan, with and without the workspace; a single TMEM accumulator over all of K fails the
+    tolerance here, so this pins the split cap."""
+    p = synth.make_structured("unit", M + 3, M=M, N=N, K=K, G=128)
+    cols = _cols(N, M, 56)
+    for ws in (WS, None):
+        y = run(p, workspace=ws)
+        _sampled_cols_check(p, y, cols)
+
+
+def test_workspace_graph_captured_before_a_larger_eager_call():
+    """No hidden allocation: capture a small-M graph, run larger-M calls eagerly with the same
+    workspace, replay the graph: bit-identical to the pre-capture eager result (round-1 bug: the
+    library grew and freed a per-stream workspace that captured graphs still pointed to)."""
+    G = 128
+    p1 = synth.make_problem(41, M=4, N=4096, K=4096, G=G)
+    p2 = synth.make_problem(42, M=64, N=28672, K=8192, G=G)
+    x1, b1, x2, b2 = to_dev_f16(p1.x), pack_dev(p1), to_dev_f16(p2.x), pack_dev(p2)
+    ws = torch.zeros(quick.quick_workspace_bytes(64, 28672, 8192, G) + (1 << 20), dtype=torch.uint8, device=DEV)
+    ref = quick.quick_w4a16_gemm(x1, b1, 4096, 4096, G, workspace=ws)
+    s = torch.cuda.Stream()
+    y = torch.empty_like(ref)
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            quick.quick_w4a16_gemm(x1, b1, 4096, 4096, G, out=y, workspace=ws)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        big = quick.quick_w4a16_gemm(x2, b2, 28672, 8192, G, workspace=ws)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(torch.int16), ref.view(torch.int16))
+    _sampled_cols_check(p2, big, _cols(28672, 5, 40))
+    # the plan is a function of the arguments only: same bits eagerly and captured without a workspace
+    y0 = quick.quick_w4a16_gemm(x1, b1, 4096, 4096, G)
+    y1 = torch.empty_like(y0)
+    with torch.cuda.stream(s):
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=s):
+            quick.quick_w4a16_gemm(x1, b1, 4096, 4096, G, out=y1)
+        g2.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+
+
+def test_graphs_replayed_concurrently_on_two_streams():
+    """Two stream-K graphs replayed at the same time on two streams, each with its own workspace
+    (quick.h: concurrent launches must not share one): both results correct and bit-identical to
+    serial launches."""
+    G = 128
+    probs = [synth.make_problem(50 + i, M=8, N=28672, K=8192, G=G) for i in range(2)]
+    xs = [to_dev_f16(p.x) for p in probs]
+    bs = [pack_dev(p) for p in probs]
+    wss = [torch.zeros(quick.quick_workspace_bytes(8, 28672, 8192, G), dtype=torch.uint8, device=DEV)
+           for _ in range(2)]
+    assert wss[0].numel() > 0
+    refs = [quick.quick_w4a16_gemm(xs[i], bs[i], 28672, 8192, G, workspace=wss[i]) for i in range(2)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [[torch.empty_like(refs[i]) for _ in range(4)] for i in range(2)]
+    graphs = []
+    for i in range(2):
+        with torch.cuda.stream(streams[i]):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=streams[i]):
+                for o in outs[i]:
+                    quick.quick_w4a16_gemm(xs[i], bs[i], 28672, 8192, G, out=o, pdl=True, workspace=wss[i])
+            graphs.append(g)
+    torch.cuda.synchronize()
+    for _ in range(5):
+        for i in range(2):
+            with torch.cuda.stream(streams[i]):
+                graphs[i].replay()
+    torch.cuda.synchronize()
+    for i in range(2):
+        for o in outs[i]:
+            assert torch.equal(o.view(torch.int16), refs[i].view(torch.int16))
+    _sampled_cols_check(probs[0], refs[0], _cols(28672, 9, 40))
+    # every launch left its workspace's arrival counters at zero
+    for w in wss:
+        ntiles = 28672 // 128
+        assert int(w[: 4 * ntiles].view(torch.int32).abs().sum().item()) == 0

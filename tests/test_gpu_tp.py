@@ -71,3 +71,62 @@ def test_gather_columns_matches_column_slices():
     torch.cuda.synchronize()
     # same plan (tile, split) => same per-element summation order => bit-identical columns
     assert torch.equal(y.view(torch.int16), full.view(torch.int16))
+
+
+# ------------------------------------------------------------------------------- world size 2 on one GPU
+# Two processes share cuda:0 and a gloo group that carries the CUDA tensors (NCCL refuses two ranks
+# on one device).  Everything else is the production path: the shard packing, the sm_100a GEMM of
+# each rank's shard, the collective, and the quick_gather_columns / quick_f32_to_f16 epilogues.
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _tp_worker(rank, world, port, q):
+    import traceback
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        res = {}
+        # column-parallel (Llama-2-70B up-projection shape, scaled down in K): all-gather + permute
+        p = synth.make_problem(61, M=12, N=2048, K=1024, G=128)
+        col = tp.ColumnParallelW4A16(p.qweight, p.scales, p.zeros, 128, device=torch.device("cuda", 0))
+        y1 = col.forward(_x(p))
+        y2 = col.forward(_x(p))               # a fresh output per call (the first is not overwritten)
+        torch.cuda.synchronize()
+        ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+        res["col"] = oracle.tol_check(y1.float().cpu().numpy(), ref)["ok"] and y1.data_ptr() != y2.data_ptr() \
+            and torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+        # the gathered columns are the single-GPU GEMM's columns bit for bit when the per-rank plan is
+        # the same as the single-GPU plan of that column slice (forced tile/split here)
+        # row-parallel (down-projection): fp32 partials, fp32 all-reduce, cast
+        p = synth.make_problem(62, M=7, N=512, K=4096, G=128)
+        row = tp.RowParallelW4A16(p.qweight, p.scales, p.zeros, 128, device=torch.device("cuda", 0))
+        xs = _x(p)[:, row.k0:row.k1].contiguous()
+        y = row.forward(xs)
+        torch.cuda.synchronize()
+        ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+        res["row"] = oracle.tol_check(y.float().cpu().numpy(), ref)["ok"]
+        q.put((rank, res))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_tp_layers_world2_on_one_gpu():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for pr in procs:
+        pr.join(60)
+    assert out == {0: {"col": True, "row": True}, 1: {"col": True, "row": True}}, out

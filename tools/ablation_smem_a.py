@@ -13,6 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402  (tools: parity of the ablation variant)
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 ABL = 1 << 21
 G = 128
@@ -52,9 +54,9 @@ for (M, N, K, tn, sk) in cases:
     y0 = torch.empty((M, N), device="cuda", dtype=torch.float16)
     y1 = torch.empty_like(y0)
     h = stream.cuda_stream
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y0.data_ptr(), h,
+    _ws.gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y0.data_ptr(), h,
                                quick.QUICK_FLAG_NO_STREAMK, tn, sk)
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y1.data_ptr(), h, ABL, tn, sk)
+    _ws.gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y1.data_ptr(), h, ABL, tn, sk)
     torch.cuda.synchronize()
     same = bool(torch.equal(y0.view(torch.int16), y1.view(torch.int16)))
     cols = np.arange(0, N, max(1, N // 256))[:256]
@@ -66,9 +68,9 @@ for (M, N, K, tn, sk) in cases:
     tol_tmem = oracle.tol_check(y0.float().cpu().numpy()[:, cols], ref)
     tol_smem = oracle.tol_check(y1.float().cpu().numpy()[:, cols], ref)
     diff = (y0.float() - y1.float()).abs().max().item()
-    t_tmem = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+    t_tmem = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                           y0.data_ptr(), h, quick.QUICK_FLAG_NO_STREAMK, tn, sk))
-    t_smem = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+    t_smem = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                           y1.data_ptr(), h, ABL, tn, sk))
     # context only: cuBLAS fp16 GEMM on the dequantized weights (4x the weight bytes), rotating copies
     wd = quick.quick_dequant_weights(blob, K, N, G)

@@ -11,6 +11,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 G = 128
 stream = torch.cuda.Stream()
@@ -52,13 +54,13 @@ for (N, K) in [(4096, 4096), (13824, 5120), (28672, 8192)]:
         x = torch.from_numpy(synth.make_x(M, M, K).view(np.int16)).view(torch.float16).cuda()
         y = torch.empty((M, N), device="cuda", dtype=torch.float16)
         h = stream.cuda_stream
-        t_q = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+        t_q = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                            y.data_ptr(), h))
         t_c = timeit(lambda i: torch.matmul(x, wds[i % nW], out=y))
         F = 2 * M * N * K
         rec = {"N": N, "K": K, "M": M, "us_quick": round(t_q, 3), "us_cublas_fp16_dense": round(t_c, 3),
                "quick_tensor_frac": round(F / t_q / 1e6 / TC, 4), "cublas_tensor_frac": round(F / t_c / 1e6 / TC, 4),
-               "plan": quick.quick_gemm_plan(M, N, K, G)}
+               "plan": _ws.plan(M, N, K, G)}
         out.write(json.dumps(rec) + "\n")
         print(rec, flush=True)
     del copies, wds, wd

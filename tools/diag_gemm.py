@@ -11,6 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "diag")
 os.makedirs(out, exist_ok=True)
@@ -25,7 +27,7 @@ for kind, M, N, K, G, tn, sk in cases:
         p = synth.make_problem(1, M, N, K, G) if kind == "random" else synth.make_structured(kind, 1, M, N, K, G)
         blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).to(dev)
         x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).to(dev)
-        y = quick.quick_w4a16_gemm(x, blob, N, K, G, tile_n=tn, split_k=sk)
+        y = _ws.gemm(x, blob, N, K, G, tile_n=tn, split_k=sk)
         torch.cuda.synchronize()
         ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, G)
         yn = y.float().cpu().numpy()

@@ -11,6 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 M, N, K, G = 256, 8192, 28672, 128
 p = synth.make_problem(M + N, M=M, N=N, K=K, G=G)
@@ -39,6 +41,6 @@ stats(emu, "emulated fp32 (16-k chunks)")
 blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).cuda()
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 for tn, sk in ((256, 1), (256, 2), (256, 4), (256, 8), (64, 1), (16, 1), (16, 8)):
-    y = quick.quick_w4a16_gemm(x, blob, N, K, G, tile_n=tn, split_k=sk, out_fp32=True)
+    y = _ws.gemm(x, blob, N, K, G, tile_n=tn, split_k=sk, out_fp32=True)
     torch.cuda.synchronize()
     stats(y.cpu().numpy()[:, cols].astype(np.float64), f"gpu tile={tn} split={sk} fp32out")

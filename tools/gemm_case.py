@@ -9,6 +9,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 M, N, K = (int(v) for v in sys.argv[1:4])
 flags = int(sys.argv[4], 0)
@@ -24,12 +26,12 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 h = stream.cuda_stream
 try:
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y.data_ptr(), h, flags, tn, sk)
+    _ws.gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y.data_ptr(), h, flags, tn, sk)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=stream):
         for i in range(16):
-            quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, 128, y.data_ptr(), h, flags,
+            _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, 128, y.data_ptr(), h, flags,
                                        tn, sk)
     g.replay()
     torch.cuda.synchronize()

@@ -11,6 +11,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 DBG_NOCOMPUTE = 1 << 30
 DBG_EXIT_TOP = 1 << 29
@@ -68,9 +70,9 @@ for (M, N, K) in shapes:
                              ("nosplit", 16, 1, 0), ("nomma", 0, 0, DBG_NO_MMA), ("onecta", 0, 0, DBG_ONE_CTA),
                              ("onecta-nocomp", 0, 0, DBG_ONE_CTA | DBG_NOCOMPUTE), ("onecta-nomma", 0, 0, DBG_ONE_CTA | DBG_NO_MMA)]:
         try:
-            t = timeit(lambda i: quick.quick_w4a16_gemm_raw(xp, copies[i % R].data_ptr(), M, N, K, G, yp, h,
+            t = timeit(lambda i: _ws.gemm_raw(xp, copies[i % R].data_ptr(), M, N, K, G, yp, h,
                                                             flags=fl, tile_n=tn, split_k=sk))
             res.append(f"{name} {t:.2f}")
         except Exception as e:  # noqa: BLE001
             res.append(f"{name} err {str(e)[:40]}")
-    print(f"M={M} N={N} K={K} plan={quick.quick_gemm_plan(M, N, K, G)} hbm-floor {wb / 6.65e3 / 1e3 * 1e3:.2f} us :: " + " | ".join(res))
+    print(f"M={M} N={N} K={K} plan={_ws.plan(M, N, K, G)} hbm-floor {wb / 6.65e3 / 1e3 * 1e3:.2f} us :: " + " | ".join(res))

@@ -9,6 +9,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 DBG = 1 << 30
 stream = torch.cuda.Stream()
@@ -44,7 +46,7 @@ for (M, N, K) in SHAPES:
     y = torch.empty((M, N), device="cuda", dtype=torch.float16)
     wb = blob.numel()
     # warm the stream-K workspace outside capture
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y.data_ptr(), stream.cuda_stream)
+    _ws.gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, 128, y.data_ptr(), stream.cuda_stream)
     for name, flags, tn, sk, hot in [("full sk", 0, 0, 0, 0), ("nocompute sk", DBG, 0, 0, 0),
                                      ("full cluster", 4, 0, 0, 0), ("nocompute cluster", DBG | 4, 0, 0, 0),
                                      ("nomma sk", 1 << 27, 0, 0, 0), ("nosttm sk", 1 << 25, 0, 0, 0),
@@ -52,7 +54,7 @@ for (M, N, K) in SHAPES:
                                      ("nosttm sk L2-hot", 1 << 25, 0, 0, 1), ("nocompute sk L2-hot", DBG, 0, 0, 1)]:
         if hot and wb > 60e6:
             continue   # does not stay in L2
-        us = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[0 if hot else i % R].data_ptr(), M, N,
+        us = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[0 if hot else i % R].data_ptr(), M, N,
                                                           K, 128, y.data_ptr(), stream.cuda_stream, flags, tn, sk))
         print(f"{M}x{N}x{K} {name:18s} {us:8.2f} us  {wb / us / 1e3:7.1f} GB/s ({wb / us / 1e3 / 6547:.3f} of HBM)",
               flush=True)

@@ -14,6 +14,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 M, N, K, tn, sk = (int(v) for v in sys.argv[1:6])
 pdl = quick.QUICK_FLAG_PDL if len(sys.argv) > 6 and sys.argv[6] == "pdl" else 0
@@ -28,7 +30,7 @@ h = stream.cuda_stream
 
 
 def run(flags, y):
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y.data_ptr(), h, flags, tn, sk)
+    _ws.gemm_raw(x.data_ptr(), blob.data_ptr(), M, N, K, G, y.data_ptr(), h, flags, tn, sk)
 
 
 tag = f"{M}x{N}x{K} tile {tn} split {sk}{' pdl' if pdl else ''}"
@@ -52,7 +54,7 @@ try:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for i in range(16):
-                quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G, y1.data_ptr(), h, fl,
+                _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G, y1.data_ptr(), h, fl,
                                            tn, sk)
         g.replay()
         torch.cuda.synchronize()

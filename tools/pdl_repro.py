@@ -11,6 +11,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 M, N, K = (int(v) for v in sys.argv[1:4])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 20
@@ -23,13 +25,13 @@ copies = [blob] + [blob.clone() for _ in range(ncopies - 1)]
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((M, N), device="cuda", dtype=torch.float16)
 if ref_first:
-    quick.quick_w4a16_gemm(x, blob, N, K, 128, out=y)
+    _ws.gemm(x, blob, N, K, 128, out=y)
     torch.cuda.synchronize()
-print("plan", quick.quick_gemm_plan(M, N, K, 128), "flags", hex(flags), flush=True)
+print("plan", _ws.plan(M, N, K, 128), "flags", hex(flags), flush=True)
 s = torch.cuda.current_stream().cuda_stream
 for r in range(reps):
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[r % ncopies].data_ptr(), M, N, K, 128, y.data_ptr(), s, flags)
+    _ws.gemm_raw(x.data_ptr(), copies[r % ncopies].data_ptr(), M, N, K, 128, y.data_ptr(), s, flags)
 torch.cuda.synchronize()
-y_ref = quick.quick_w4a16_gemm(x, blob, N, K, 128)
+y_ref = _ws.gemm(x, blob, N, K, 128)
 torch.cuda.synchronize()
 print("ok, bit-equal to a non-PDL launch:", bool(torch.equal(y, y_ref)), flush=True)

@@ -10,6 +10,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--M", type=int, default=1)
@@ -28,10 +30,10 @@ x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((a.M, a.N), device="cuda", dtype=torch.float16)
 for r in range(a.reps):
     if a.flags:
-        quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[r].data_ptr(), a.M, a.N, a.K, a.G, y.data_ptr(),
+        _ws.gemm_raw(x.data_ptr(), copies[r].data_ptr(), a.M, a.N, a.K, a.G, y.data_ptr(),
                                    torch.cuda.current_stream().cuda_stream, flags=a.flags, tile_n=a.tile_n,
                                    split_k=a.split_k)
     else:
-        quick.quick_w4a16_gemm(x, copies[r], a.N, a.K, a.G, out=y, tile_n=a.tile_n, split_k=a.split_k)
+        _ws.gemm(x, copies[r], a.N, a.K, a.G, out=y, tile_n=a.tile_n, split_k=a.split_k)
 torch.cuda.synchronize()
-print("plan", quick.quick_gemm_plan(a.M, a.N, a.K, a.G))
+print("plan", _ws.plan(a.M, a.N, a.K, a.G))

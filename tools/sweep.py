@@ -15,6 +15,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 SHAPES = {"small": [(4096, 4096)],
           "big": [(28672, 8192), (8192, 28672)],
@@ -70,7 +72,7 @@ for (N, K) in SHAPES[which]:
         y = torch.empty((M, N), device=dev, dtype=torch.float16)
         B = K * N // 2 + (K // G) * N * 5 // 2 + 2 * M * K + 2 * M * N
         F = 2 * M * N * K
-        rec = {"N": N, "K": K, "M": M, "plan": quick.quick_gemm_plan(M, N, K, G)}
+        rec = {"N": N, "K": K, "M": M, "plan": _ws.plan(M, N, K, G)}
         for mode in modes:
             # "auto" / "pdl" / "nosk", or a forced plan "t<tile>s<split>[p]" (e.g. t256s2, t256s2p)
             fl, tn, sk = FLAGS.get(mode, 0), 0, 0
@@ -81,7 +83,7 @@ for (N, K) in SHAPES[which]:
                 tn, sk = (int(v) for v in mode[1:].rstrip("p").split("s"))
                 if tn > 2 * M and tn > 16:
                     continue
-            us = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+            us = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                               y.data_ptr(), stream.cuda_stream, fl, tn, sk))
             rec[mode] = {"us": round(us, 3), "hbm": round(B / (us * 1e-6) / HBM, 4),
                          "tc": round(F / (us * 1e-6) / TC, 4)}

@@ -10,6 +10,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 M, N, K = (int(v) for v in sys.argv[1:4])
 tn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
@@ -23,12 +25,12 @@ blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G
 copies = [blob.clone() for _ in range(max(4, int(3e8 // blob.numel())))]
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((M, N), device="cuda", dtype=torch.float16)
-NCTA = quick.quick_gemm_plan(M, N, K, G)["num_ctas"] if not (tn or sk) else 4096
+NCTA = _ws.plan(M, N, K, G)["num_ctas"] if not (tn or sk) else 4096
 tr = torch.zeros(16 * STRIDE + 3 * max(NCTA, 4096), dtype=torch.int64, device="cuda")
 
 
 def run(w):
-    quick.quick_w4a16_gemm_raw(x.data_ptr(), w.data_ptr(), M, N, K, G, y.data_ptr(), 0, FLAGS, tn, sk)
+    _ws.gemm_raw(x.data_ptr(), w.data_ptr(), M, N, K, G, y.data_ptr(), 0, FLAGS, tn, sk)
 
 
 for i in range(3):
@@ -71,7 +73,7 @@ if len(rec):
     slow = idx[d_all > 2 * np.median(d_all)]
     print("slow CTAs (lin idx, smid, start us, dur us):",
           [(int(i), int(full[i, 0]), round((full[i, 1] - t0) / 1e3, 2), round((full[i, 2] - full[i, 1]) / 1e3, 2)) for i in slow[:20]])
-print("plan", quick.quick_gemm_plan(M, N, K, G), "tile", tn, "split", sk)
+print("plan", _ws.plan(M, N, K, G), "tile", tn, "split", sk)
 names = ["P_before_empty", "P_issued", "D_full", "D_aempty_ok", "D_afull_arrived", "M_afull_ok", "M_committed"]
 for c in range(16):
     row = t[c]

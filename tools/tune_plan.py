@@ -11,6 +11,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2402_10076_b200 import quick  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 OUT = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "tune.jsonl")
 shapes = [(4096, 4096), (13824, 5120), (5120, 13824), (28672, 8192), (8192, 28672)]
@@ -54,7 +56,7 @@ for (N, K) in shapes:
     for M in Ms:
         x = torch.from_numpy(synth.make_x(M, M, K).view(np.int16)).view(torch.float16).to(dev)
         y = torch.empty((M, N), device=dev, dtype=torch.float16)
-        auto = quick.quick_gemm_plan(M, N, K, G)
+        auto = _ws.plan(M, N, K, G)
         cover = 16 if M <= 16 else 32 if M <= 32 else 64 if M <= 64 else 128 if M <= 128 else 256
         results = []
         for tn in (16, 32, 64, 128, 256):
@@ -64,14 +66,14 @@ for (N, K) in shapes:
                 if sk > K // 64:
                     continue
                 try:
-                    us = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+                    us = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                                       y.data_ptr(), stream.cuda_stream, 0, tn, sk))
                 except Exception as e:  # noqa
                     us = None
                 results.append((tn, sk, us))
-        us_auto = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+        us_auto = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                                y.data_ptr(), stream.cuda_stream))
-        us_pdl = timeit(lambda i: quick.quick_w4a16_gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+        us_pdl = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                               y.data_ptr(), stream.cuda_stream, quick.QUICK_FLAG_PDL))
         ok = [r for r in results if r[2] is not None]
         best = min(ok, key=lambda r: r[2])
