@@ -55,6 +55,34 @@ quick_status_t quick_pack_weights(const uint32_t* qweight, const uint16_t* scale
                                   const uint32_t* zeros, int group_size, int K, int N,
                                   void* packed_out);
 
+/* Fused gate||up repack (host, the MLP's two column-parallel projections as one GEMM
+ * whose epilogue applies SiLU(gate) * up, QUICK_FLAG_SILU_MUL).  Inputs: the gate and the up
+ * projection, each in the AWQ format above with I output columns (qweight [K][I/8], scales
+ * [K/G][I], zeros [K/G][I/8]).  Output: the v1 blob of the N = 2I column matrix W' whose column
+ * 128t + 32q + l is gate column 64t + 16q + l for l < 16 and up column 64t + 16q + l - 16 for
+ * l >= 16 (a gate row and its up row sit in TMEM lanes l and l + 16 of one warp, so the epilogue
+ * pairs them with one shuffle).  packed_out: quick_packed_bytes(K, 2I, G) bytes.
+ * Requires I % 64 == 0 (else QUICK_ERR_UNSUPPORTED). */
+quick_status_t quick_pack_gate_up(const uint32_t* qweight_gate, const uint16_t* scales_gate,
+                                  const uint32_t* zeros_gate, const uint32_t* qweight_up,
+                                  const uint16_t* scales_up, const uint32_t* zeros_up,
+                                  int group_size, int K, int I, void* packed_out);
+
+/* GPTQ checkpoint import (host; the GPTQ family of P:L19).  Input, the AutoGPTQ
+ * format: qweight uint32 [K/8][N] with nibble i of word (j, n) = code of row 8j + i; qzeros uint32
+ * [K/G][N/8] with nibble i of word (g, j) = zero of column 8j + i minus zero_plus_one (1 for the
+ * classic "v1" checkpoints that store zero - 1, 0 for "v2"); scales fp16 bits [K/G][N]; g_idx
+ * int32 [K] = group of row k (act-order / desc_act checkpoints permute rows across groups; NULL =
+ * k / G).  Output: the same weights in the AWQ format above (qweight_awq [K][N/8], scales_out
+ * [K/G][N], zeros_awq [K/G][N/8]) with the rows reordered so that group g is rows [gG, (g+1)G):
+ * row k' of the output is source row perm[k'] (perm int32 [K], identity when g_idx is NULL or
+ * monotone), so Y = X . W = X[:, perm] . W_out (quick_gather_k permutes X on the device).
+ * QUICK_ERR_UNSUPPORTED if a group does not hold exactly G rows or a decoded zero is 16. */
+quick_status_t quick_import_gptq(const uint32_t* qweight, const uint32_t* qzeros, const uint16_t* scales,
+                                 const int32_t* g_idx, int zero_plus_one, int group_size, int K, int N,
+                                 uint32_t* qweight_awq, uint16_t* scales_out, uint32_t* zeros_awq,
+                                 int32_t* perm);
+
 /* Exact inverse of quick_pack_weights (host). Same array shapes as above, written completely. */
 quick_status_t quick_unpack_weights(const void* packed, int group_size, int K, int N,
                                     uint32_t* qweight, uint16_t* scales, uint32_t* zeros);
@@ -81,6 +109,11 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
                                 also dequantized before that point.  Ignored by plans with
                                 256-token tiles. */
 #define QUICK_FLAG_NO_STREAMK 4 /* never use the stream-K schedule (tests / A-B timing) */
+#define QUICK_FLAG_SILU_MUL 8   /* fused gate||up epilogue for a blob made by
+                                   quick_pack_gate_up: Y is __half [M][N/2] (ldy >= N/2) with
+                                   Y[m][i] = fp16_rne(SiLU(G[m][i]) * U[m][i]), G = X.gate and
+                                   U = X.up accumulated in fp32, SiLU(g) = g / (1 + exp(-g)) in
+                                   fp32.  Not with QUICK_FLAG_OUT_F32. */
 
 /* Bytes of caller-owned workspace the call quick_w4a16_gemm_ex(M, N, K, G, flags, tile_n,
  * split_k) can use: the small-M stream-K schedule (tiles of <= 64 tokens) keeps one fp32
@@ -120,6 +153,17 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
 quick_status_t quick_gemm_plan(int M, int N, int K, int group_size, int flags,
                                size_t workspace_bytes, int* tile_n, int* split_k, int* num_ctas,
                                int* cta_pair);
+
+/* quick_pack_weights on the device (repack of 70B-scale checkpoints at HBM speed):
+ * the same AWQ tensors and the same v1 blob, bit-exact, all pointers device memory (packed_out
+ * 16-byte aligned, quick_packed_bytes bytes).  Asynchronous on `stream`. */
+quick_status_t quick_pack_weights_device(const uint32_t* qweight, const uint16_t* scales,
+                                         const uint32_t* zeros, int group_size, int K, int N,
+                                         void* packed_out, void* stream);
+
+/* Activation side of a GPTQ act-order import: Xp[m][k'] = X[m][perm[k']] (device __half [M][K],
+ * perm device int32 [K] from quick_import_gptq).  Asynchronous on `stream`. */
+quick_status_t quick_gather_k(const void* X, const int32_t* perm, int M, int K, void* Xp, void* stream);
 
 /* Device dequantization of a packed blob into W fp16 [K][N] row-major (device), computing
  * dequant(q)[k][n] bit-exactly as fp16_rne((q - z) * s) (§2.3).  Asynchronous. */

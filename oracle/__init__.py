@@ -18,6 +18,8 @@ from .quick_oracle import (  # noqa: F401
     gemm,
     w4a16_reference,
     round_fp16,
+    silu_mul,
+    gptq_dequant,
     tol_check,
     v1_packed_bytes,
     v1_weight_pos,

@@ -22,6 +22,15 @@ What the path computes (PAPER.md = /root/reference/PAPER.md, "P:L<n>" = its line
               form of §3.2): an independent encoder/decoder written from the layout
               text, used to check the library packer bit-for-bit.
 
+  O8 gptq     (GPTQ is the P:L19 family): dequantization of an AutoGPTQ
+              checkpoint, w[k][n] = fp16_rne((q[k][n] - z[g_idx[k]][n]) * s[g_idx[k]][n]),
+              q packed 8 rows per word (nibble i = row 8j + i), z packed 8 columns per word
+              (nibble i = column 8j + i) and stored as z - 1 in "v1" checkpoints (R17).
+  O7 silu_mul (the fused gate||up epilogue; not in PAPER.md, whose MLP is
+              not on its hot path -- DESIGN.md reading R16): h = SiLU(g) * u with
+              SiLU(g) = g / (1 + exp(-g)) (the Llama/Mistral MLP activation), in fp64 on the
+              two O3 results.
+
 No blocking, fusion or reordering beyond the definitions above; numpy's fp64 matmul is the
 one library primitive used (as a step: a dot product in fp64).
 """
@@ -84,6 +93,35 @@ def gemm(x: np.ndarray, w: np.ndarray) -> np.ndarray:
 def w4a16_reference(x, qweight, scales, zeros, group_size) -> np.ndarray:
     """O1 -> O2 -> O3: the fp64 reference of Y = X . dequant(Wq)."""
     return gemm(x, dequant(qweight, scales, zeros, group_size))
+
+
+# ----------------------------------------------------------------------------------------- O8
+def gptq_dequant(qweight, qzeros, scales, g_idx=None, group_size=None, zero_plus_one=True) -> np.ndarray:
+    """O8: fp16 [K][N] weights of an AutoGPTQ checkpoint (R17)."""
+    qweight = np.asarray(qweight).view(np.uint32)
+    qzeros = np.asarray(qzeros).view(np.uint32)
+    K, N = qweight.shape[0] * 8, qweight.shape[1]
+    q = np.empty((K, N), dtype=np.int64)
+    for i in range(8):                                  # row 8j + i in nibble i
+        q[i::8, :] = (qweight >> np.uint32(4 * i)) & np.uint32(0xF)
+    NG = qzeros.shape[0]
+    z = np.empty((NG, N), dtype=np.int64)
+    for i in range(8):                                  # column 8j + i in nibble i
+        z[:, i::8] = (qzeros >> np.uint32(4 * i)) & np.uint32(0xF)
+    if zero_plus_one:
+        z = z + 1
+    g = np.arange(K) // group_size if g_idx is None else np.asarray(g_idx, dtype=np.int64)
+    s = np.asarray(scales, dtype=np.float16).astype(np.float64)
+    return ((q - z[g, :]).astype(np.float64) * s[g, :]).astype(np.float16)
+
+
+# ----------------------------------------------------------------------------------------- O7
+def silu_mul(g: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """O7: SiLU(g) * u = g / (1 + exp(-g)) * u in fp64 (R16)."""
+    g = np.asarray(g, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    with np.errstate(over="ignore"):
+        return g / (1.0 + np.exp(-g)) * u
 
 
 # ----------------------------------------------------------------------------------------- O4

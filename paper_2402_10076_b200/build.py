@@ -7,7 +7,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libquick.so")
-SOURCES = [os.path.join(CSRC, "quick_gemm.cu"), os.path.join(CSRC, "quick_pack.cpp")]
+SOURCES = [os.path.join(CSRC, "quick_gemm.cu"), os.path.join(CSRC, "quick_repack.cu"), os.path.join(CSRC, "quick_pack.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "quick_ptx.cuh"), os.path.join(ROOT, "include", "quick.h")]
 
 NVCC_FLAGS = [

@@ -56,7 +56,8 @@ constexpr int kDebugExitPrologue = 1 << 28;  // debug: return after the prologue
 constexpr int kDebugNoMma = 1 << 27;       // debug: dequant + STTM but no MMA (commits only)
 constexpr int kDebugOneCta = 1 << 26;      // debug: stream-K with one CTA per SM (smem padded)
 constexpr int kDebugNoSttm = 1 << 25;      // debug: dequant into registers, no TMEM store, no MMA
-constexpr int kDebugPdlEarly = 1 << 24;    // debug: PDL trigger right after the prologue
+constexpr int kDebugPdlEarly = 1 << 24;    // PDL trigger right after the prologue (set by the host for
+                                           // stream-K grids that fill every CTA slot; forcible for tests)
 constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memory (Cfg AM = 1)
 constexpr int kForcePair = 1 << 20;        // debug: CTA-pair (cta_group::2) plan for tiles 128/256
 constexpr int kDebugNoPair = 1 << 19;      // debug: automatic plan without CTA pairs
@@ -283,6 +284,11 @@ __device__ __forceinline__ void dequant_word(uint32_t w, const DequantConsts& c,
   out[3] = hmul2_rn(hfma2_rn(hi1, kInv16, c.zhi), c.s2);
 }
 
+// SiLU(g) * u in fp32 (the fused gate||up epilogue, QUICK_FLAG_SILU_MUL)
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  return g * __frcp_rn(1.0f + __expf(-g)) * u;
+}
+
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), version 1
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
   uint64_t d = 0;
@@ -336,6 +342,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   const int C32 = K / 32;
   const int NG = K / G;
   const bool out_fp32 = (p.flags & QUICK_FLAG_OUT_F32) != 0;
+  // fused gate||up (quick_pack_gate_up): TMEM lanes l < 16 and l + 16 of each warp hold a gate row
+  // and its up row; Y[m][n'] = SiLU(gate) * up with n' = 64 t + 16 q + l, stored by lanes l < 16
+  const bool silu = (p.flags & QUICK_FLAG_SILU_MUL) != 0;
   const bool pdl = (p.flags & QUICK_FLAG_PDL) != 0;
   const bool dbg_nocompute = (p.flags & kDebugNoCompute) != 0;   // load path only (debug)
   const bool dbg_nosttm = (p.flags & kDebugNoSttm) != 0;
@@ -881,7 +890,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       if (!it.more()) ptx::griddep_launch_dependents();   // our last segment: CTA finishing
       const int db = SK ? (si & 1) : 0;
       const int m0 = sg.mt * BN;
-      const int n = sg.t * kTileRows + r;
+      const int n = silu ? sg.t * (kTileRows / 2) + q * 16 + (lane & 15) : sg.t * kTileRows + r;
+      const bool silu_store = (lane & 16) == 0;
       ptx::mbar_wait(bar_dfull + 8 * db, (uint32_t)((si >> 1) & 1));
       ptx::tc_fence_after();
       if (TRACE && tr != nullptr && warp == 0 && lane == 0) tr[1] = clock64();
@@ -921,7 +931,16 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       };
       // 8 tokens (columns jc .. jc + 7, the first `cnt` valid) of this thread's output column n
       auto store_y8 = [&](int jc, const float (&f)[8], int cnt) {
-        if (out_fp32) {
+        if (silu) {   // warp-uniform: every lane shuffles, the gate lanes store
+          __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float u = __shfl_xor_sync(0xffffffffu, f[i], 16);
+            if (i < cnt && silu_store) *yp = __float2half_rn(silu_mul(f[i], u));
+            yp += p.ldy;
+            asm volatile("" : "+l"(yp));
+          }
+        } else if (out_fp32) {
           float* yp = reinterpret_cast<float*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -952,7 +971,17 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           const int cnt = jmax - jc;   // valid tokens in this chunk (>= 32: all)
           // (the pointer is made opaque after each bump so that the compiler does not keep 32
           // precomputed 64-bit addresses live)
-          if (out_fp32) {
+          if (silu) {
+            __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float g = __uint_as_float(v[i]);
+              const float u = __shfl_xor_sync(0xffffffffu, g, 16);
+              if (i < cnt && silu_store) *yp = __float2half_rn(silu_mul(g, u));
+              yp += p.ldy;
+              asm volatile("" : "+l"(yp));
+            }
+          } else if (out_fp32) {
             float* yp = reinterpret_cast<float*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
@@ -1138,7 +1167,31 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           }
       }
     };
-    if (S == 2) {
+    if (silu) {
+      // fused gate||up: whole tokens per CTA (token-aligned split) so that each gate float4 (rows
+      // rr..rr+3, rr % 32 < 16) and its up float4 (rows rr+16..) are reduced by the same CTA; sum
+      // order q = 0..S-1 as below
+      const int tb = ((int)my * BN) / S;
+      const int te = min((((int)my + 1) * BN) / S, max(0, M - m0));
+      for (int i = (int)threadIdx.x; i < (te - tb) * 16; i += kThreads) {
+        const int j = tb + (i >> 4);
+        const int rr = ((i >> 2) & 3) * 32 + (i & 3) * 4;
+        const int eg = j * kTileRows + rr;
+        float4 g = load_part(0, eg), u = load_part(0, eg + 16);
+        for (int qq = 1; qq < S; ++qq) {
+          const float4 g2 = load_part(qq, eg), u2 = load_part(qq, eg + 16);
+          g.x += g2.x; g.y += g2.y; g.z += g2.z; g.w += g2.w;
+          u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
+        }
+        __half2 lo = __floats2half2_rn(silu_mul(g.x, u.x), silu_mul(g.y, u.y));
+        __half2 hi = __floats2half2_rn(silu_mul(g.z, u.z), silu_mul(g.w, u.w));
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * (kTileRows / 2) + (rr >> 5) * 16 + (rr & 15);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
+      }
+    } else if (S == 2) {
       reduce_unrolled(std::integral_constant<int, 2>{});
     } else if (S == 3) {
       reduce_unrolled(std::integral_constant<int, 3>{});
@@ -1726,7 +1779,8 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   return QUICK_OK;
 }
 
-constexpr int kKnownFlags = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | quick::kDebugNoCompute |
+constexpr int kKnownFlags = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | QUICK_FLAG_SILU_MUL |
+                            quick::kDebugNoCompute |
                             quick::kDebugExitTop | quick::kDebugExitPrologue | quick::kDebugNoMma |
                             quick::kDebugOneCta | quick::kDebugNoSttm | quick::kDebugPdlEarly |
                             quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair | quick::kDebugForceSk;
@@ -1783,6 +1837,10 @@ bool x_tensor_map(const void* X, int M, int K, int rows, int kc, CUtensorMap* ou
 inline bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 }  // namespace
+
+namespace quick {
+void set_last_cuda_error(int e) { g_last_cuda_error = e; }
+}  // namespace quick
 
 extern "C" {
 
@@ -1842,8 +1900,11 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   if (st != QUICK_OK) return st;
   if (M == 0) return QUICK_OK;
   if (!X || !packed || !Y) return QUICK_ERR_INVALID_ARG;
-  if (ldy < N) return QUICK_ERR_INVALID_ARG;
+  // fused gate||up: Y has N / 2 columns (SiLU(gate) * up), fp16 only
+  const bool silu = (flags & QUICK_FLAG_SILU_MUL) != 0;
+  if (ldy < (silu ? N / 2 : N)) return QUICK_ERR_INVALID_ARG;
   if (ldy % 8 != 0 || (flags & ~kKnownFlags) != 0) return QUICK_ERR_UNSUPPORTED;
+  if (silu && (flags & (QUICK_FLAG_OUT_F32 | quick::kAblationSmemA))) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (workspace_bytes != 0 && (workspace == nullptr || !aligned(workspace, 256))) return QUICK_ERR_INVALID_ARG;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1890,6 +1951,13 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
   // the 256-token tile launches without programmatic dependent launch (an
   // intermittent fault with deeper PDL prefetch whose root cause is not established)
   kp.flags = (tn == 256) ? (flags & ~QUICK_FLAG_PDL) : flags;
+  // A stream-K grid holding every CTA slot of the machine triggers its dependents right after the
+  // prologue: the next GEMM's CTAs can only land in slots our CTAs vacate, so an early trigger
+  // lets each one start (prologue, weight prefetch, first dequantized stages) as soon as a slot
+  // frees instead of after our slowest CTA reaches its epilogue (tools/sweep.py pdl vs pdlearly on
+  // B200: 28672x8192 M = 1 31.1 -> 30.4 us).  Grids smaller than the machine keep the late trigger
+  // (an early one lets the next grid double up on busy SMs).
+  if (plan.sk && (kp.flags & QUICK_FLAG_PDL) && plan.P >= max_resident(tn, true, 1)) kp.flags |= quick::kDebugPdlEarly;
   kp.NA = NA;
   kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;

@@ -106,6 +106,90 @@ quick_status_t quick_pack_weights(const uint32_t* qweight, const uint16_t* scale
   return QUICK_OK;
 }
 
+quick_status_t quick_pack_gate_up(const uint32_t* qw_g, const uint16_t* sc_g, const uint32_t* z_g,
+                                  const uint32_t* qw_u, const uint16_t* sc_u, const uint32_t* z_u, int G,
+                                  int K, int I, void* packed_out) {
+  if (!qw_g || !sc_g || !z_g || !qw_u || !sc_u || !z_u || !packed_out) return QUICK_ERR_INVALID_ARG;
+  if (I <= 0 || I % 8 != 0) return QUICK_ERR_INVALID_ARG;
+  if (I % 64 != 0) return QUICK_ERR_UNSUPPORTED;
+  const int N = 2 * I;
+  quick_status_t st = check_shape(K, N, G);
+  if (st != QUICK_OK) return st;
+  // the interleaved AWQ tensors of W' (column map in quick.h), then the ordinary v1 repack
+  const int NG = K / G, WPR = N / 8, WPR_I = I / 8;
+  auto src_col = [](int n, bool* up) {   // W' column n -> (gate/up, source column)
+    const int t = n / 128, q = (n % 128) / 32, l = n % 32;
+    *up = l >= 16;
+    return 64 * t + 16 * q + (l & 15);
+  };
+  std::vector<uint32_t> qw((size_t)K * WPR, 0u), zr((size_t)NG * WPR, 0u);
+  std::vector<uint16_t> sc((size_t)NG * N);
+  parallel_for(N / 8, [&](int j) {   // one AWQ word column of W' per task (no shared words)
+    for (int o = 0; o < 8; ++o) {
+      const int n = 8 * j + o;
+      bool up;
+      const int c = src_col(n, &up);
+      const uint32_t* qsrc = up ? qw_u : qw_g;
+      const uint32_t* zsrc = up ? z_u : z_g;
+      const uint16_t* ssrc = up ? sc_u : sc_g;
+      for (int k = 0; k < K; ++k) qw[(size_t)k * WPR + j] |= awq_code(qsrc, k, c, WPR_I) << (4 * kAwqSlot[o]);
+      for (int g = 0; g < NG; ++g) {
+        zr[(size_t)g * WPR + j] |= awq_code(zsrc, g, c, WPR_I) << (4 * kAwqSlot[o]);
+        sc[(size_t)g * N + n] = ssrc[(size_t)g * I + c];
+      }
+    }
+  });
+  return quick_pack_weights(qw.data(), sc.data(), zr.data(), G, K, N, packed_out);
+}
+
+quick_status_t quick_import_gptq(const uint32_t* qweight, const uint32_t* qzeros, const uint16_t* scales,
+                                 const int32_t* g_idx, int zero_plus_one, int G, int K, int N,
+                                 uint32_t* qweight_awq, uint16_t* scales_out, uint32_t* zeros_awq, int32_t* perm) {
+  if (!qweight || !qzeros || !scales || !qweight_awq || !scales_out || !zeros_awq || !perm)
+    return QUICK_ERR_INVALID_ARG;
+  if (K <= 0 || N <= 0 || G <= 0 || K % G != 0 || K % 8 != 0 || N % 8 != 0) return QUICK_ERR_INVALID_ARG;
+  const int NG = K / G, WPR = N / 8;
+  // row order of the imported matrix: rows sorted by group (stable), so every group is G
+  // consecutive rows (GPTQ act-order permutes the rows of each group across K)
+  std::vector<int> count(NG, 0);
+  for (int k = 0; k < K; ++k) {
+    const int g = g_idx ? g_idx[k] : k / G;
+    if (g < 0 || g >= NG) return QUICK_ERR_INVALID_ARG;
+    ++count[g];
+  }
+  for (int g = 0; g < NG; ++g)
+    if (count[g] != G) return QUICK_ERR_UNSUPPORTED;   // not G rows per group: no v1 group structure
+  std::vector<int> next(NG);
+  for (int g = 0; g < NG; ++g) next[g] = g * G;
+  for (int k = 0; k < K; ++k) perm[next[g_idx ? g_idx[k] : k / G]++] = k;
+  // zeros: GPTQ packs (z - zero_plus_one) along N in natural nibble order; a decoded zero of 16
+  // (v1 checkpoints storing 15) has no 4-bit representation
+  std::memset(zeros_awq, 0, (size_t)NG * WPR * 4);
+  for (int g = 0; g < NG; ++g)
+    for (int n = 0; n < N; ++n) {
+      const uint32_t z = ((qzeros[(size_t)g * WPR + (n >> 3)] >> (4 * (n & 7))) & 0xFu) + (zero_plus_one ? 1u : 0u);
+      if (z > 15u) return QUICK_ERR_UNSUPPORTED;
+      zeros_awq[(size_t)g * WPR + (n >> 3)] |= z << (4 * kAwqSlot[n & 7]);
+    }
+  std::memcpy(scales_out, scales, (size_t)NG * N * sizeof(uint16_t));
+  // codes: GPTQ packs 8 rows per word (nibble i = row 8j + i); AWQ packs 8 columns per word
+  parallel_for(K / 8, [&](int kb) {
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k2 = 8 * kb + kk;   // row of the imported matrix
+      const int k = perm[k2];       // source row
+      uint32_t* dst = qweight_awq + (size_t)k2 * WPR;
+      const uint32_t* src = qweight + (size_t)(k >> 3) * N;
+      const int sh = 4 * (k & 7);
+      for (int j = 0; j < WPR; ++j) {
+        uint32_t word = 0;
+        for (int o = 0; o < 8; ++o) word |= ((src[8 * j + o] >> sh) & 0xFu) << (4 * kAwqSlot[o]);
+        dst[j] = word;
+      }
+    }
+  });
+  return QUICK_OK;
+}
+
 quick_status_t quick_unpack_weights(const void* packed, int G, int K, int N, uint32_t* qweight,
                                     uint16_t* scales, uint32_t* zeros) {
   if (!packed || !qweight || !scales || !zeros) return QUICK_ERR_INVALID_ARG;

@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libquick.so")
 
 QUICK_OK, QUICK_ERR_INVALID_ARG, QUICK_ERR_UNSUPPORTED, QUICK_ERR_CUDA = 0, 1, 2, 3
-QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL, QUICK_FLAG_NO_STREAMK = 1, 2, 4
+QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL, QUICK_FLAG_NO_STREAMK, QUICK_FLAG_SILU_MUL = 1, 2, 4, 8
 
 
 class QuickError(RuntimeError):
@@ -33,6 +33,13 @@ def _load():
         "quick_packed_bytes": (c_size_t, [c_int, c_int, c_int]),
         "quick_pack_weights": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
         "quick_unpack_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+        "quick_import_gptq": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p,
+                                      c_void_p, c_void_p, c_void_p]),
+        "quick_pack_weights_device": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p,
+                                              c_void_p]),
+        "quick_gather_k": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+        "quick_pack_gate_up": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                       c_int, c_void_p]),
         "quick_w4a16_gemm": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
         "quick_w4a16_gemm_ex": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int,
                                         c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
@@ -110,6 +117,97 @@ def quick_pack_weights(qweight, scales, zeros, group_size: int) -> np.ndarray:
     return out[:nbytes]
 
 
+def _awq_checked(qweight, scales, zeros, group_size):
+    qweight, scales, zeros = np.asarray(qweight), np.asarray(scales), np.asarray(zeros)
+    if qweight.ndim != 2 or qweight.dtype not in (np.uint32, np.int32):
+        raise ValueError(f"qweight must be a 2-D uint32/int32 array [K][N/8], got {qweight.dtype} {qweight.shape}")
+    K, N = qweight.shape[0], qweight.shape[1] * 8
+    if group_size <= 0 or K % group_size:
+        raise ValueError(f"group_size {group_size} must divide K={K}")
+    if scales.dtype not in (np.float16, np.uint16) or scales.shape != (K // group_size, N):
+        raise ValueError(f"scales must be float16 (K/G, N) = {(K // group_size, N)}, got {scales.dtype} {scales.shape}")
+    if zeros.dtype not in (np.uint32, np.int32) or zeros.shape != (K // group_size, N // 8):
+        raise ValueError(f"zeros must be uint32/int32 (K/G, N/8) = {(K // group_size, N // 8)}, "
+                         f"got {zeros.dtype} {zeros.shape}")
+    return (np.ascontiguousarray(qweight).view(np.uint32), np.ascontiguousarray(scales).view(np.uint16),
+            np.ascontiguousarray(zeros).view(np.uint32), K, N)
+
+
+def quick_pack_gate_up(gate, up, group_size: int) -> np.ndarray:
+    """Fused gate||up blob (quick.h): gate / up = (qweight, scales, zeros) AWQ tuples with I columns each;
+    the GEMM with QUICK_FLAG_SILU_MUL on it returns SiLU(X.gate) * (X.up) [M][I]."""
+    qg, sg, zg, K, I = _awq_checked(*gate, group_size)
+    qu, su, zu, K2, I2 = _awq_checked(*up, group_size)
+    if (K2, I2) != (K, I):
+        raise ValueError(f"gate {K}x{I} and up {K2}x{I2} shapes differ")
+    nbytes = quick_packed_bytes(K, 2 * I, group_size)
+    out = np.empty(max(nbytes, 1), dtype=np.uint8)
+    _check("quick_pack_gate_up", _lib.quick_pack_gate_up(_np_ptr(qg), _np_ptr(sg), _np_ptr(zg), _np_ptr(qu),
+                                                         _np_ptr(su), _np_ptr(zu), group_size, K, I, _np_ptr(out)))
+    return out[:nbytes]
+
+
+def quick_import_gptq(qweight, qzeros, scales, group_size: int, g_idx=None, zero_plus_one: bool = True):
+    """AutoGPTQ tensors (qweight [K/8][N], qzeros [K/G][N/8] storing zero - zero_plus_one, scales fp16
+    [K/G][N], optional g_idx [K]) -> (qweight_awq, scales, zeros_awq, perm) in the AWQ format with the
+    rows sorted by group (quick.h quick_import_gptq).  Pack the result with quick_pack_weights and feed
+    the GEMM X[:, perm] (quick_gather_k) when perm is not the identity."""
+    qweight = np.ascontiguousarray(qweight).view(np.uint32)
+    qzeros = np.ascontiguousarray(qzeros).view(np.uint32)
+    scales = np.ascontiguousarray(scales)
+    K, N = qweight.shape[0] * 8, qweight.shape[1]
+    if group_size <= 0 or K % group_size:
+        raise ValueError(f"group_size {group_size} must divide K={K}")
+    if scales.dtype not in (np.float16, np.uint16) or scales.shape != (K // group_size, N):
+        raise ValueError(f"scales must be float16 (K/G, N) = {(K // group_size, N)}")
+    if qzeros.shape != (K // group_size, N // 8):
+        raise ValueError(f"qzeros must be (K/G, N/8) = {(K // group_size, N // 8)}")
+    scales = scales.view(np.uint16)
+    gi = None
+    if g_idx is not None:
+        gi = np.ascontiguousarray(g_idx, dtype=np.int32)
+        if gi.shape != (K,):
+            raise ValueError(f"g_idx must have K={K} entries")
+    qa = np.empty((K, N // 8), np.uint32)
+    sa = np.empty((K // group_size, N), np.uint16)
+    za = np.empty((K // group_size, N // 8), np.uint32)
+    perm = np.empty(K, np.int32)
+    _check("quick_import_gptq", _lib.quick_import_gptq(
+        _np_ptr(qweight), _np_ptr(qzeros), _np_ptr(scales), _np_ptr(gi) if gi is not None else None,
+        1 if zero_plus_one else 0, group_size, K, N, _np_ptr(qa), _np_ptr(sa), _np_ptr(za), _np_ptr(perm)))
+    return qa, sa.view(np.float16), za, perm
+
+
+def quick_pack_weights_device(qweight, scales, zeros, group_size: int, out=None, stream=None):
+    """quick_pack_weights on the GPU: torch cuda tensors qweight int32/uint32 [K][N/8], scales fp16 [K/G][N],
+    zeros int32 [K/G][N/8] -> the v1 blob (cuda uint8), bit-identical to the host packer."""
+    import torch
+    K, N = qweight.shape[0], qweight.shape[1] * 8
+    for t, shape in ((qweight, (K, N // 8)), (scales, (K // group_size, N)), (zeros, (K // group_size, N // 8))):
+        if not (t.is_cuda and t.is_contiguous() and tuple(t.shape) == shape and t.element_size() in (2, 4)):
+            raise ValueError(f"device AWQ tensors must be contiguous cuda tensors of shape {shape}")
+    if scales.dtype not in (torch.float16, torch.int16) or qweight.element_size() != 4 or zeros.element_size() != 4:
+        raise ValueError("qweight / zeros must be 32-bit, scales fp16")
+    nbytes = quick_packed_bytes(K, N, group_size)
+    if out is None:
+        out = torch.empty(nbytes, dtype=torch.uint8, device=qweight.device)
+    _check("quick_pack_weights_device", _lib.quick_pack_weights_device(
+        ctypes.c_void_p(qweight.data_ptr()), ctypes.c_void_p(scales.data_ptr()), ctypes.c_void_p(zeros.data_ptr()),
+        group_size, K, N, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+    return out
+
+
+def quick_gather_k(x, perm, out=None, stream=None):
+    """Xp[m][k'] = X[m][perm[k']] on the GPU (x cuda fp16 [M][K], perm cuda int32 [K])."""
+    import torch
+    M, K = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    _check("quick_gather_k", _lib.quick_gather_k(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(perm.data_ptr()), M, K,
+                                                 ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)))
+    return out
+
+
 def quick_unpack_weights(packed, group_size: int, K: int, N: int):
     """Exact inverse of quick_pack_weights -> (qweight uint32, scales fp16, zeros uint32)."""
     packed = np.ascontiguousarray(packed, dtype=np.uint8)
@@ -158,11 +256,12 @@ def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ld
         raise ValueError(f"packed has {packed.numel()} bytes, expected {quick_packed_bytes(K, N, group_size)}")
     M = x.shape[0]
     want = torch.float32 if out_fp32 else torch.float16
+    n_out = N // 2 if (flags & QUICK_FLAG_SILU_MUL) else N
     if out is None:
-        out = torch.empty((M, N), device=x.device, dtype=want)
-    elif not (out.is_cuda and out.dtype == want and out.dim() == 2 and out.shape[0] >= M and out.shape[1] >= N
+        out = torch.empty((M, n_out), device=x.device, dtype=want)
+    elif not (out.is_cuda and out.dtype == want and out.dim() == 2 and out.shape[0] >= M and out.shape[1] >= n_out
               and out.stride(1) == 1 and out.device == x.device):
-        raise ValueError(f"out must be a cuda {want} [>= {M}][>= {N}] tensor with unit column stride")
+        raise ValueError(f"out must be a cuda {want} [>= {M}][>= {n_out}] tensor with unit column stride")
     ld = out.stride(0) if ldy is None else ldy
     ws_ptr, ws_bytes = None, 0
     if workspace is not None:

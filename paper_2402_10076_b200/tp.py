@@ -50,6 +50,52 @@ def shard_awq_rows(qweight, scales, zeros, G: int, rank: int, world: int):
             np.ascontiguousarray(zeros[k0 // G:k1 // G]))
 
 
+def shard_qkv_columns(qweight, scales, zeros, n_heads: int, n_kv_heads: int, head_dim: int, rank: int, world: int):
+    """Megatron column shard of a fused QKV projection (SURVEY §8(e) semantic slicing): the AWQ
+    tensors' columns are [Q heads | K heads | V heads] (n_heads, n_kv_heads, n_kv_heads heads of
+    head_dim columns); rank r keeps its n_heads/P query heads and n_kv_heads/P key and value heads,
+    as [q_r | k_r | v_r] (so the attention of its heads needs nothing from other ranks).
+    Mistral-7B at P = 8: 4 q + 1 k + 1 v heads = 768 columns."""
+    if n_heads % world or n_kv_heads % world:
+        raise ValueError(f"heads ({n_heads} q, {n_kv_heads} kv) do not split over {world} ranks")
+    N = scales.shape[1]
+    if N != (n_heads + 2 * n_kv_heads) * head_dim:
+        raise ValueError(f"N={N} != (n_heads + 2 n_kv_heads) x head_dim")
+    hq, hk = n_heads // world, n_kv_heads // world
+    spans = [(rank * hq * head_dim, (rank + 1) * hq * head_dim)]
+    off = n_heads * head_dim
+    spans.append((off + rank * hk * head_dim, off + (rank + 1) * hk * head_dim))
+    off += n_kv_heads * head_dim
+    spans.append((off + rank * hk * head_dim, off + (rank + 1) * hk * head_dim))
+    for a, b in spans:
+        if a % 8 or b % 8:
+            raise ValueError("head_dim must keep shard spans on AWQ word boundaries")
+    n_r = sum(b - a for a, b in spans)
+    if n_r % 128:
+        raise ValueError(f"per-rank QKV width {n_r} is not a multiple of 128 (v1 layout)")
+    cat = np.concatenate
+    return (np.ascontiguousarray(cat([qweight[:, a // 8:b // 8] for a, b in spans], axis=1)),
+            np.ascontiguousarray(cat([scales[:, a:b] for a, b in spans], axis=1)),
+            np.ascontiguousarray(cat([zeros[:, a // 8:b // 8] for a, b in spans], axis=1)))
+
+
+def shard_gate_up(gate, up, rank: int, world: int):
+    """Megatron column shard of the MLP's gate and up projections: rank r keeps the
+    same I/P columns of both (its slice of the intermediate activation), packed together with
+    quick_pack_gate_up so one GEMM + SiLU*mul epilogue produces that slice."""
+    I = gate[1].shape[1]
+    if I % (64 * world):
+        raise ValueError(f"I={I} is not a multiple of 64 x world ({world}): no fused gate||up shard")
+    i_r = I // world
+    c0, c1 = rank * i_r, (rank + 1) * i_r
+
+    def cut(t):
+        qw, sc, zr = t
+        return (np.ascontiguousarray(qw[:, c0 // 8:c1 // 8]), np.ascontiguousarray(sc[:, c0:c1]),
+                np.ascontiguousarray(zr[:, c0 // 8:c1 // 8]))
+    return cut(gate), cut(up)
+
+
 # ----------------------------------------------------------------------------------- layers
 class ColumnParallelW4A16:
     """Y[M, N] = X[M, K] . dequant(Wq)[K, N], N split across the process group."""
@@ -126,3 +172,64 @@ class RowParallelW4A16:
         self.dist.all_reduce(partial, op=self.dist.ReduceOp.SUM, group=self.group)   # fp32 on the wire
         self.quick.quick_f32_to_f16(partial, dst=y)
         return y
+
+
+class MegatronMLP:
+    """The MLP linear stack in the Megatron split (BASELINE.json configs[4]):
+    fused gate||up column-parallel GEMM with the SiLU*mul epilogue (QUICK_FLAG_SILU_MUL) producing
+    this rank's I/P slice of the activation, then the row-parallel down projection (fp32 partial,
+    fp32 all-reduce, cast).  No collective between the two GEMMs."""
+
+    def __init__(self, gate, up, down, group_size: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from . import quick
+        self.quick, self.torch = quick, torch
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.G, self.K = group_size, gate[0].shape[0]
+        g_r, u_r = shard_gate_up(gate, up, rank, world)
+        self.I_r = g_r[1].shape[1]
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.gate_up = torch.from_numpy(quick.quick_pack_gate_up(g_r, u_r, group_size)).to(self.device)
+        self.down = RowParallelW4A16(*down, group_size, group=group, device=self.device)
+        if self.down.Kr != self.I_r or self.down.k0 != rank * self.I_r:
+            raise ValueError("down projection rows must match this rank's intermediate slice")
+        self.workspace = None
+
+    def forward(self, x, out=None):
+        h = self.quick.quick_w4a16_gemm(x, self.gate_up, 2 * self.I_r, self.K, self.G,
+                                        flags=self.quick.QUICK_FLAG_SILU_MUL, workspace=self.workspace)
+        self.down.workspace = self.workspace
+        return self.down.forward(h, out=out)
+
+
+class MegatronAttentionProjections:
+    """QKV column-parallel by head group (this rank's heads, no collective) and the O projection
+    row-parallel over the same heads (fp32 all-reduce); attention itself is not on the hot path
+    (SURVEY §8(d)), so `forward_o` takes this rank's attention output [M, n_heads/P x head_dim]."""
+
+    def __init__(self, qkv, o, n_heads: int, n_kv_heads: int, head_dim: int, group_size: int, group=None,
+                 device=None):
+        import torch
+        import torch.distributed as dist
+        from . import quick
+        self.quick = quick
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.G, self.K = group_size, qkv[0].shape[0]
+        q_r = shard_qkv_columns(*qkv, n_heads, n_kv_heads, head_dim, rank, world)
+        self.N_r = q_r[1].shape[1]
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.qkv = torch.from_numpy(quick.quick_pack_weights(*q_r, group_size)).to(self.device)
+        self.o = RowParallelW4A16(*o, group_size, group=group, device=self.device)
+        if self.o.Kr != (n_heads // world) * head_dim:
+            raise ValueError("O projection rows must match this rank's query heads")
+        self.workspace = None
+
+    def forward_qkv(self, x, out=None):
+        return self.quick.quick_w4a16_gemm(x, self.qkv, self.N_r, self.K, self.G, out=out, workspace=self.workspace)
+
+    def forward_o(self, attn_r, out=None):
+        self.o.workspace = self.workspace
+        return self.o.forward(attn_r, out=out)

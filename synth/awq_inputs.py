@@ -104,3 +104,29 @@ def make_structured(kind: str, seed: int, M: int, N: int, K: int, G: int = 128) 
     else:
         raise ValueError(f"unknown structured set {kind!r}")
     return p
+
+
+@dataclass
+class GPTQProblem:
+    """One problem in the AutoGPTQ checkpoint format (random bits only): qweight [K/8][N] packed along
+    K, qzeros [K/G][N/8] packed along N, scales fp16 [K/G][N], g_idx [K] (act-order: a seeded random
+    permutation of the rows' groups, each group holding G rows)."""
+    x: np.ndarray
+    qweight: np.ndarray
+    qzeros: np.ndarray
+    scales: np.ndarray
+    g_idx: np.ndarray
+    group_size: int
+
+
+def make_gptq_problem(seed: int, M: int, N: int, K: int, G: int = 128, act_order: bool = True) -> GPTQProblem:
+    x = make_x(seed, M, K)
+    qweight = _words(seed, T_QWEIGHT, K // 8, N)
+    # zeros stored as z - 1 ("v1"): keep the decoded zero in [1, 15] so it has a 4-bit form
+    qzeros = _words(seed, T_ZEROS, K // G, N // 8) & np.uint32(0xEEEEEEEE)
+    scales = make_scales(seed, K, N, G)
+    g_idx = np.arange(K, dtype=np.int32) // G
+    if act_order:
+        order = np.argsort(splitmix64(_stream_seed(seed, 9), K), kind="stable")
+        g_idx = g_idx[order].astype(np.int32)
+    return GPTQProblem(x, qweight, qzeros, scales, g_idx, G)

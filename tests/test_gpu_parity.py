@@ -580,3 +580,54 @@ def test_graphs_replayed_concurrently_on_two_streams():
     for w in wss:
         ntiles = 28672 // 128
         assert int(w[: 4 * ntiles].view(torch.int32).abs().sum().item()) == 0
+
+
+# ------------------------------------------------------------------------------- fused gate||up + SiLU (f2)
+def _silu_ref(x, pg, pu, cols=None):
+    G = pg.group_size
+    def part(p):
+        if cols is None:
+            return oracle.w4a16_reference(x, p.qweight, p.scales, p.zeros, G)
+        q = oracle.unpack_awq(p.qweight)[:, cols]
+        z = oracle.unpack_awq(p.zeros)[:, cols]
+        w = oracle.dequant(oracle.pack_awq(q), p.scales[:, cols], oracle.pack_awq(z), G)
+        return oracle.gemm(x, w)
+    return oracle.silu_mul(part(pg), part(pu))
+
+
+@pytest.mark.parametrize("M,K,I,tile_n,split_k", [(8, 512, 128, 0, 0), (5, 1024, 256, 16, 3), (33, 1024, 256, 64, 2),
+                                                  (16, 2048, 256, 16, 0), (100, 2048, 320, 128, 1),
+                                                  (130, 1024, 256, 128, 4), (300, 1024, 192, 256, 2),
+                                                  (200, 1024, 512, 0, 0), (1, 4096, 1024, 0, 0)])
+def test_fused_gate_up_silu(M, K, I, tile_n, split_k):
+    """QUICK_FLAG_SILU_MUL on a quick_pack_gate_up blob = SiLU(X.gate) * (X.up) (oracle O7 on the two O3
+    results) within the tolerance, across the plan families: stream-K (workspace), cluster split-K
+    (token-aligned DSMEM reduce), whole tiles of 16..256 tokens, CTA pairs (auto, M = 200)."""
+    G = 128 if K % 128 == 0 else 64
+    pg = synth.make_problem(M + K + I, M=M, N=I, K=K, G=G)
+    pu = synth.make_problem(M + K + I + 1, M=M, N=I, K=K, G=G)
+    blob = torch.from_numpy(quick.quick_pack_gate_up((pg.qweight, pg.scales, pg.zeros),
+                                                     (pu.qweight, pu.scales, pu.zeros), G)).to(DEV)
+    x = to_dev_f16(pg.x)
+    y = quick.quick_w4a16_gemm(x, blob, 2 * I, K, G, flags=quick.QUICK_FLAG_SILU_MUL, tile_n=tile_n,
+                               split_k=split_k, workspace=WS)
+    torch.cuda.synchronize()
+    assert y.shape == (M, I)
+    res = oracle.tol_check(y.float().cpu().numpy(), _silu_ref(pg.x, pg, pu))
+    assert res["ok"], res
+
+
+@pytest.mark.parametrize("M", [1, 16, 64, 256])
+def test_fused_gate_up_silu_mistral_shape(M):
+    """Mistral-7B gate_up (K = 4096, I = 14336) through the automatic plan with PDL, sampled columns."""
+    K, I, G = 4096, 14336, 128
+    pg = synth.make_problem(900 + M, M=M, N=I, K=K, G=G)
+    pu = synth.make_problem(901 + M, M=M, N=I, K=K, G=G)
+    blob = torch.from_numpy(quick.quick_pack_gate_up((pg.qweight, pg.scales, pg.zeros),
+                                                     (pu.qweight, pu.scales, pu.zeros), G)).to(DEV)
+    y = quick.quick_w4a16_gemm(to_dev_f16(pg.x), blob, 2 * I, K, G, flags=quick.QUICK_FLAG_SILU_MUL, pdl=True,
+                               workspace=WS)
+    torch.cuda.synchronize()
+    cols = _cols(I, M, 96)
+    res = oracle.tol_check(y.float().cpu().numpy()[:, cols], _silu_ref(pg.x, pg, pu, cols))
+    assert res["ok"], res

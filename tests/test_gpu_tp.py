@@ -110,6 +110,34 @@ def _tp_worker(rank, world, port, q):
         torch.cuda.synchronize()
         ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
         res["row"] = oracle.tol_check(y.float().cpu().numpy(), ref)["ok"]
+        # Megatron MLP (BASELINE.json configs[4] split): fused gate||up + SiLU epilogue on this rank's
+        # intermediate slice, straight into the row-parallel down projection, one fp32 all-reduce
+        K, I, G = 1024, 512, 128
+        pg = synth.make_problem(63, M=9, N=I, K=K, G=G)
+        pu = synth.make_problem(64, M=9, N=I, K=K, G=G)
+        pdn = synth.make_problem(65, M=9, N=K, K=I, G=G)
+        mlp = tp.MegatronMLP((pg.qweight, pg.scales, pg.zeros), (pu.qweight, pu.scales, pu.zeros),
+                             (pdn.qweight, pdn.scales, pdn.zeros), G, device=torch.device("cuda", 0))
+        y = mlp.forward(_x(pg))
+        torch.cuda.synchronize()
+        h = oracle.round_fp16(oracle.silu_mul(oracle.w4a16_reference(pg.x, pg.qweight, pg.scales, pg.zeros, G),
+                                              oracle.w4a16_reference(pg.x, pu.qweight, pu.scales, pu.zeros, G)))
+        ref = oracle.w4a16_reference(h, pdn.qweight, pdn.scales, pdn.zeros, G)
+        res["mlp"] = oracle.tol_check(y.float().cpu().numpy(), ref)["ok"]
+        # attention projections: QKV by head group (8 q + 2 kv heads of 128), O row-parallel
+        nh, nkv, hd = 8, 2, 128
+        pq = synth.make_problem(66, M=5, N=(nh + 2 * nkv) * hd, K=1024, G=G)
+        po = synth.make_problem(67, M=5, N=1024, K=nh * hd, G=G)
+        att = tp.MegatronAttentionProjections((pq.qweight, pq.scales, pq.zeros), (po.qweight, po.scales, po.zeros),
+                                              nh, nkv, hd, G, device=torch.device("cuda", 0))
+        qkv_r = att.forward_qkv(_x(pq))
+        o = att.forward_o(_x(po)[:, att.o.k0:att.o.k1].contiguous())
+        torch.cuda.synchronize()
+        q_r = tp.shard_qkv_columns(pq.qweight, pq.scales, pq.zeros, nh, nkv, hd, rank, world)
+        ok_qkv = oracle.tol_check(qkv_r.float().cpu().numpy(), oracle.w4a16_reference(pq.x, *q_r, G))["ok"]
+        ok_o = oracle.tol_check(o.float().cpu().numpy(),
+                                oracle.w4a16_reference(po.x, po.qweight, po.scales, po.zeros, G))["ok"]
+        res["attn"] = ok_qkv and ok_o
         q.put((rank, res))
     except Exception:
         q.put((rank, traceback.format_exc()))
@@ -129,4 +157,5 @@ def test_tp_layers_world2_on_one_gpu():
     out = dict(q.get(timeout=600) for _ in procs)
     for pr in procs:
         pr.join(60)
-    assert out == {0: {"col": True, "row": True}, 1: {"col": True, "row": True}}, out
+    want = {"col": True, "row": True, "mlp": True, "attn": True}
+    assert out == {0: want, 1: want}, out

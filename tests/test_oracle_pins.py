@@ -319,3 +319,29 @@ def test_synth_ranges_and_determinism():
     s = p.scales.astype(np.float64)
     assert s.min() >= 0.0039 and s.max() <= 0.0121
     assert p.qweight.dtype == np.uint32 and p.qweight.shape == (512, 32)
+
+
+# ------------------------------------------------------------------ O7 silu_mul (R16)
+def test_silu_mul_closed_forms():
+    """SiLU(0) = 0; SiLU(1) = 1 / (1 + e^-1) (decimal value of the logistic function at 1, computed
+    here with the standard-library exp, not numpy); SiLU(x) - SiLU(-x) = x for every x (since
+    sigmoid(x) + sigmoid(-x) = 1); SiLU(x) -> x for large x and -> 0 for very negative x; and the
+    factor u enters linearly."""
+    import math
+    assert oracle.silu_mul(0.0, 5.0) == 0.0
+    assert abs(oracle.silu_mul(1.0, 1.0) - 1.0 / (1.0 + math.exp(-1.0))) < 1e-15
+    assert abs(oracle.silu_mul(1.0, 1.0) - 0.7310585786300049) < 1e-15
+    x = np.linspace(-12, 12, 97)
+    np.testing.assert_allclose(oracle.silu_mul(x, 1.0) - oracle.silu_mul(-x, 1.0), x, rtol=0, atol=1e-12)
+    assert abs(oracle.silu_mul(40.0, 1.0) - 40.0) < 1e-12
+    assert abs(oracle.silu_mul(-40.0, 1.0)) < 1e-15
+    np.testing.assert_allclose(oracle.silu_mul(x, 3.0), 3.0 * oracle.silu_mul(x, 1.0), rtol=1e-15)
+
+
+def test_silu_mul_against_torch():
+    """The library statement of the same activation: torch.nn.functional.silu in float64."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3)
+    g, u = rng.normal(0, 4, 1000), rng.normal(0, 1, 1000)
+    ref = (torch.nn.functional.silu(torch.from_numpy(g)) * torch.from_numpy(u)).numpy()
+    np.testing.assert_allclose(oracle.silu_mul(g, u), ref, rtol=1e-13, atol=1e-300)

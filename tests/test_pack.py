@@ -79,3 +79,38 @@ def test_pack_rejects_bad_shapes():
     qw = np.zeros((100, 16), dtype=np.uint32)
     with pytest.raises(quick.QuickError):
         quick.quick_pack_weights(qw, np.zeros((1, 128), np.float16), np.zeros((1, 16), np.uint32), 100)
+
+
+def _gate_up_columns(cg, cu, I):
+    """W' of quick.h's quick_pack_gate_up, written independently: column 128t + 32q + l is gate
+    column 64t + 16q + l (l < 16) or up column 64t + 16q + l - 16 (l >= 16)."""
+    out = np.empty((cg.shape[0], 2 * I), dtype=cg.dtype)
+    for n in range(2 * I):
+        t, q, l = n // 128, (n % 128) // 32, n % 32
+        src = cu if l >= 16 else cg
+        out[:, n] = src[:, 64 * t + 16 * q + (l % 16)]
+    return out
+
+
+@pytest.mark.parametrize("K,I,G", [(256, 64, 64), (512, 192, 128), (128, 320, 32)])
+def test_pack_gate_up_matches_oracle_encoder(K, I, G):
+    """The fused gate||up blob is the v1 blob of the interleaved matrix W' (the oracle's independent
+    v1 encoder applied to W' built column by column here), bit for bit."""
+    pg = synth.make_problem(K + I, M=1, N=I, K=K, G=G)
+    pu = synth.make_problem(K + I + 1, M=1, N=I, K=K, G=G)
+    blob = quick.quick_pack_gate_up((pg.qweight, pg.scales, pg.zeros), (pu.qweight, pu.scales, pu.zeros), G)
+    codes = _gate_up_columns(oracle.unpack_awq(pg.qweight), oracle.unpack_awq(pu.qweight), I)
+    zeros = _gate_up_columns(oracle.unpack_awq(pg.zeros), oracle.unpack_awq(pu.zeros), I)
+    scales = _gate_up_columns(pg.scales.view(np.uint16), pu.scales.view(np.uint16), I).view(np.float16)
+    ref = oracle.pack_v1(oracle.pack_awq(codes), scales, oracle.pack_awq(zeros), G, K, 2 * I)
+    assert np.array_equal(blob, ref)
+
+
+def test_pack_gate_up_rejects_bad_shapes():
+    pg = synth.make_problem(1, M=1, N=96, K=128, G=64)   # I = 96: not a multiple of 64
+    with pytest.raises(quick.QuickError):
+        quick.quick_pack_gate_up((pg.qweight, pg.scales, pg.zeros), (pg.qweight, pg.scales, pg.zeros), 64)
+    pu = synth.make_problem(1, M=1, N=128, K=128, G=64)
+    pg = synth.make_problem(1, M=1, N=64, K=128, G=64)
+    with pytest.raises(ValueError):
+        quick.quick_pack_gate_up((pg.qweight, pg.scales, pg.zeros), (pu.qweight, pu.scales, pu.zeros), 64)

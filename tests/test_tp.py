@@ -119,3 +119,53 @@ def test_fp16_partials_would_break_the_tolerance():
     y32 = sum(pp.astype(np.float32).astype(np.float64) for pp in parts)
     assert not oracle.tol_check(y16, ref)["ok"]
     assert oracle.tol_check(y32, ref)["ok"]
+
+
+# ------------------------------------------------------------------ Megatron semantic slicing (configs[4])
+def test_qkv_shard_keeps_whole_heads():
+    """Scales encode the column index, so the shard's columns can be read back: rank r holds query
+    heads [r nh/P, (r+1) nh/P), then its key heads, then its value heads (Mistral-7B ratio 4:1)."""
+    nh, nkv, hd, K, G = 8, 2, 128, 256, 128
+    N = (nh + 2 * nkv) * hd
+    p = synth.make_problem(7, M=1, N=N, K=K, G=G)
+    scales = np.tile(np.arange(N, dtype=np.float16)[None, :], (K // G, 1))   # exact up to 2048
+    for world in (1, 2):
+        cols = []
+        for r in range(world):
+            qw, sc, zr = tp.shard_qkv_columns(p.qweight, scales, p.zeros, nh, nkv, hd, r, world)
+            got = sc[0].astype(np.int64)
+            hq, hk = nh // world, nkv // world
+            want = np.concatenate([np.arange(r * hq * hd, (r + 1) * hq * hd),
+                                   nh * hd + np.arange(r * hk * hd, (r + 1) * hk * hd),
+                                   (nh + nkv) * hd + np.arange(r * hk * hd, (r + 1) * hk * hd)])
+            assert np.array_equal(got, want)
+            codes = oracle.unpack_awq(qw)
+            assert np.array_equal(codes, oracle.unpack_awq(p.qweight)[:, want])
+            assert np.array_equal(oracle.unpack_awq(zr), oracle.unpack_awq(p.zeros)[:, want])
+            cols.append(want)
+        assert np.array_equal(np.sort(np.concatenate(cols)), np.arange(N))
+    with pytest.raises(ValueError):
+        tp.shard_qkv_columns(p.qweight, scales, p.zeros, nh, nkv, hd, 0, 4)   # 2 kv heads over 4 ranks
+
+
+def _mlp_tp(rank, world):
+    """Megatron MLP on CPU (oracle GEMMs): each rank's fused gate||up slice feeds its down rows
+    directly; the fp32 all-reduce of the down partials equals the full MLP."""
+    K, I, G = 512, 256, 128
+    pg = synth.make_problem(31, M=4, N=I, K=K, G=G)
+    pu = synth.make_problem(32, M=4, N=I, K=K, G=G)
+    pdn = synth.make_problem(33, M=4, N=K, K=I, G=G)
+    g_r, u_r = tp.shard_gate_up((pg.qweight, pg.scales, pg.zeros), (pu.qweight, pu.scales, pu.zeros), rank, world)
+    h_r = oracle.round_fp16(oracle.silu_mul(oracle.w4a16_reference(pg.x, *g_r, G), oracle.w4a16_reference(pg.x, *u_r, G)))
+    d_r = tp.shard_awq_rows(pdn.qweight, pdn.scales, pdn.zeros, G, rank, world)
+    part = torch.from_numpy(oracle.w4a16_reference(h_r, *d_r, G))
+    dist.all_reduce(part, op=dist.ReduceOp.SUM)
+    h = oracle.round_fp16(oracle.silu_mul(oracle.w4a16_reference(pg.x, pg.qweight, pg.scales, pg.zeros, G),
+                                          oracle.w4a16_reference(pg.x, pu.qweight, pu.scales, pu.zeros, G)))
+    ref = oracle.w4a16_reference(h, pdn.qweight, pdn.scales, pdn.zeros, G)
+    return float(np.max(np.abs(part.numpy() - ref)))
+
+
+def test_megatron_mlp_slicing_gloo_world2():
+    res = run_world(_mlp_tp)
+    assert all(isinstance(v, float) and v < 1e-9 for v in res.values()), res

@@ -43,8 +43,10 @@ def timeit(launch, L=16, reps=5):
     return float(np.median(ts))
 
 
-cases = [(16, 4096, 4096, 16, 4), (16, 28672, 8192, 16, 1), (128, 4096, 4096, 128, 4), (512, 4096, 4096, 128, 1),
-         (1024, 28672, 8192, 128, 1)]
+# argv: cases "MxNxKxTILExSPLIT,..." (default: the round-1 set)
+cases = [tuple(int(v) for v in c.split("x")) for c in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
+    [(16, 4096, 4096, 16, 4), (16, 28672, 8192, 16, 1), (128, 4096, 4096, 128, 4), (512, 4096, 4096, 128, 1),
+     (1024, 28672, 8192, 128, 1)]
 for (M, N, K, tn, sk) in cases:
     p = synth.make_problem(0, M, N, K, G)
     blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).cuda()

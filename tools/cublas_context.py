@@ -20,6 +20,8 @@ torch.cuda.set_stream(stream)
 out = open(os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "cublas_context.jsonl"), "a")
 TC = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                  "MEASURED_PEAKS.json")))["bf16_tflops"]
+HBM = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                  "MEASURED_PEAKS.json")))["hbm_gbs"]
 
 
 def timeit(launch, L=16, reps=5):
@@ -42,7 +44,11 @@ def timeit(launch, L=16, reps=5):
     return float(np.median(ts))
 
 
-for (N, K) in [(4096, 4096), (13824, 5120), (28672, 8192)]:
+# argv: shapes "NxK,NxK" and M points "1,16,..." (default: the round-1 context set)
+SHAPES = [tuple(int(v) for v in s.split("x")) for s in sys.argv[1].split(",")] if len(sys.argv) > 1 else \
+    [(4096, 4096), (13824, 5120), (28672, 8192)]
+MS = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [16, 128, 256, 512, 1024]
+for (N, K) in SHAPES:
     p = synth.make_problem(0, 1, N, K, G)
     blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).cuda()
     R = max(2, int(np.ceil(300e6 / blob.numel())))
@@ -50,16 +56,21 @@ for (N, K) in [(4096, 4096), (13824, 5120), (28672, 8192)]:
     wd = quick.quick_dequant_weights(blob, K, N, G)
     nW = max(2, int(np.ceil(300e6 / (wd.numel() * 2))))
     wds = [wd] + [wd.clone() for _ in range(nW - 1)]
-    for M in (16, 128, 256, 512, 1024):
+    for M in MS:
         x = torch.from_numpy(synth.make_x(M, M, K).view(np.int16)).view(torch.float16).cuda()
         y = torch.empty((M, N), device="cuda", dtype=torch.float16)
         h = stream.cuda_stream
         t_q = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
                                                            y.data_ptr(), h))
+        t_p = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
+                                             y.data_ptr(), h, flags=quick.QUICK_FLAG_PDL))
         t_c = timeit(lambda i: torch.matmul(x, wds[i % nW], out=y))
         F = 2 * M * N * K
-        rec = {"N": N, "K": K, "M": M, "us_quick": round(t_q, 3), "us_cublas_fp16_dense": round(t_c, 3),
+        B = K * N // 2 + (K // G) * N * 5 // 2 + 2 * M * K + 2 * M * N
+        rec = {"N": N, "K": K, "M": M, "us_quick": round(t_q, 3), "us_quick_pdl": round(t_p, 3),
+               "us_cublas_fp16_dense": round(t_c, 3),
                "quick_tensor_frac": round(F / t_q / 1e6 / TC, 4), "cublas_tensor_frac": round(F / t_c / 1e6 / TC, 4),
+               "quick_hbm_frac": round(B / t_q / 1e3 / HBM, 4), "speedup_vs_cublas": round(t_c / t_q, 3),
                "plan": _ws.plan(M, N, K, G)}
         out.write(json.dumps(rec) + "\n")
         print(rec, flush=True)
