@@ -156,6 +156,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ GPU arm
+def tp_desc(kind, peer):
+    if kind == "col":
+        return "column-parallel, all-gather fused into the GEMM epilogue (peer memory)" if peer else \
+            "column-parallel + NCCL all-gather"
+    if kind == "colx":
+        return "column-parallel (output stays sharded)"
+    if kind == "silu":
+        return "fused gate||up + SiLU*mul, column-parallel (output stays sharded)"
+    return "row-parallel + peer-memory fp32 all-reduce" if peer else "row-parallel + NCCL fp32 all-reduce"
+
+
 def plan_key(plan):
     """Kernel identity of a launch: the template instantiation and grid family it runs."""
     sched = "stream-K" if plan["split_k"] == 0 else f"split{plan['split_k']}"
@@ -249,6 +260,32 @@ def run_quick(args, rank, world, dist):
                                    g["y"].data_ptr(), sh, flags=fl, ws_ptr=ws_ptr, ws_bytes=ws_bytes,
                                    ldy=g["n_out"])
 
+    peer = world > 1 and args.comm == "peer"
+    if peer:
+        # collective-fused TP over peer memory: symmetric buffers (CUDA IPC, handles
+        # exchanged over the NCCL group), the column-parallel all-gather fused into the GEMM epilogue,
+        # the row-parallel fp32 all-reduce done by our own peer-memory kernel; two Y buffers per point
+        comm = tp.PeerComm()
+        for g in gemms:
+            if g["kind"] == "col":
+                g["ypeer"] = [comm.buffer(g["M"] * g["N"] * 2) for _ in range(2)]
+            elif g["kind"] == "row":
+                g["ppeer"] = comm.buffer(g["M"] * g["N"] * 4)
+                g["ypeer"] = [comm.buffer(g["M"] * g["N"] * 2) for _ in range(2)]
+            g["turn"] = 0
+
+    def launch_peer(g, slot):
+        x = g["xs"][slot % len(g["xs"])]
+        w = wcopies[g["si"]][slot]
+        yp = g["ypeer"][g["turn"]]
+        g["turn"] ^= 1
+        if g["kind"] == "col":
+            quick.quick_tp_column_gemm(x, w, g["Nl"], g["Kl"], G, yp, g["N"], comm.flags, rank,
+                                       flags=quick.QUICK_FLAG_PDL | EXTRA_FLAGS, workspace=ws)
+        else:
+            quick.quick_tp_row_gemm(x, w, g["N"], g["Kl"], G, g["ppeer"], yp, g["N"], comm.flags, rank,
+                                    flags=quick.QUICK_FLAG_PDL | EXTRA_FLAGS, workspace=ws)
+
     def collective(g):
         if world == 1 or g["kind"] in ("colx", "silu"):
             return          # colx / silu: the sharded output feeds the next (row-parallel) GEMM, no gather
@@ -260,17 +297,24 @@ def run_quick(args, rank, world, dist):
             quick.quick_f32_to_f16(g["y"], dst=g["yfull"])
 
     for g in gemms:
-        launch(g, 0)
-        collective(g)
+        if peer and g["kind"] in ("col", "row"):
+            launch_peer(g, 0)
+        else:
+            launch(g, 0)
+            collective(g)
     torch.cuda.synchronize()
 
-    # graph per GEMM point holding C launches (+ their collectives when `with_coll`)
+    # graph per GEMM point holding C launches (+ their collectives when `with_coll`; with --comm peer
+    # the collective-fused TP calls replace both)
     def build_graphs(C, with_coll):
         graphs = []
         for gi, g in enumerate(gemms):
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=stream):
                 for c in range(C):
+                    if with_coll and peer and g["kind"] in ("col", "row"):
+                        launch_peer(g, (gi * C + c) % R)
+                        continue
                     launch(g, (gi * C + c) % R)
                     if with_coll:
                         collective(g)
@@ -447,20 +491,21 @@ def run_quick(args, rank, world, dist):
         "config": {"workload": args.workload, "baseline_config": cfg_idx,
                    "shapes_NxK": [[n, k, kind] for n, k, kind in shapes], "M": Ms, "group_size": G,
                    "gemms_per_step": len(gemms),
-                   "parallelism": (f"tp{world}: " + ", ".join(
-                       f"{n}x{k} {'column-parallel + NCCL all-gather' if kind == 'col' else 'column-parallel (output stays sharded)' if kind == 'colx' else 'fused gate||up + SiLU*mul, column-parallel' if kind == 'silu' else 'row-parallel + NCCL fp32 all-reduce'}"
-                       for n, k, kind in shapes)) if world > 1 else "single GPU",
+                   "parallelism": (f"tp{world}: " + ", ".join(f"{n}x{k} {tp_desc(kind, peer)}" for n, k, kind in shapes))
+                                   if world > 1 else "single GPU",
                    "l2": (f"rotating {R} weight copies per shape ({R * blob_bytes / 2**20:.0f} MiB) > L2 "
                           f"{l2 / 2**20:.0f} MiB; every launch reads its weights from HBM") if l2_cold else
                          f"weights L2-resident ({R} copies of {blob_bytes} B < 2.5 x L2)",
                    "timing": f"CUDA-graph replays of {BLOCK_C} launches per GEMM point (PDL between consecutive "
                              "launches), point-major; events between replays"
-                             + ("; NCCL collectives captured in the graphs" if coll_in_graph else
+                             + ("; collective-fused peer-memory TP calls captured in the graphs" if peer else
+                                "; NCCL collectives captured in the graphs" if coll_in_graph else
                                 "; NCCL collectives eager after each replay" if world > 1 else ""),
                    "launch": "quick_w4a16_gemm_ex with QUICK_FLAG_PDL and a caller-owned stream-K workspace, "
                              "automatic plan"},
         "hbm_gbs_aggregate": round(K_steps * step_bytes / (elapsed_ms * 1e-3) / 1e9, 1),
-        "gpu_launches": K_steps * sum(1 + (2 if (world > 1 and g["kind"] in ("col", "row")) else 0) for g in gemms),
+        "gpu_launches": K_steps * sum((2 if g["kind"] == "col" else 4) if (peer and g["kind"] in ("col", "row")) else
+                                      1 + (2 if (world > 1 and g["kind"] in ("col", "row")) else 0) for g in gemms),
         "roofline": roof,
         "sweep": sweep,
         **({"layer_stack_32_layers": layer_stack} if layer_stack else {}),
@@ -669,6 +714,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--comm", choices=["nccl", "peer"], default="nccl",
+                    help="N > 1: NCCL collectives after the GEMMs, or the collective-fused peer-memory TP GEMMs")
     args = ap.parse_args()
     if args.warmup < 3 or args.steps < 1 or args.gpus < 1:
         sys.exit("bench.py: needs --warmup >= 3, --steps >= 1, --gpus >= 1")

@@ -178,6 +178,52 @@ quick_status_t quick_f32_to_f16(const void* src, void* dst, size_t n, void* stre
 quick_status_t quick_gather_columns(const void* src, void* dst, int P, int M, int Nr,
                                     void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Collective-fused tensor parallelism over peer memory (BASELINE.json north_star
+ * (4)).  One process per GPU.  Buffers that other ranks access are allocated with
+ * quick_peer_alloc (setup time, zeroed), exported as 64-byte handles, exchanged by the caller's
+ * process group, and mapped with quick_peer_import; a kernel then loads and stores peer memory
+ * directly (NVLink / NVSwitch; same-device IPC when the ranks share a GPU).  Per rank the caller
+ * holds arrays of world pointers, entry p = rank p's buffer as mapped in this process.
+ * Barriers use a flag array of world + 1 uint32 per rank (quick_peer_alloc'd, zeroed): slot p
+ * receives rank p's signals, slot `world` counts this rank's barriers on the device, so CUDA
+ * graphs that capture these calls replay correctly.  Every rank must issue the same sequence of
+ * TP calls on a communicator.  A barrier wait longer than 20 s traps (loud launch failure, no hang).
+ * ------------------------------------------------------------------------------------------- */
+#define QUICK_IPC_HANDLE_BYTES 64
+
+quick_status_t quick_peer_alloc(size_t bytes, void** ptr);        /* device memory, zeroed */
+quick_status_t quick_peer_free(void* ptr);
+quick_status_t quick_peer_export(const void* ptr, void* handle_out); /* QUICK_IPC_HANDLE_BYTES */
+quick_status_t quick_peer_import(const void* handle, void** ptr); /* map another rank's buffer */
+quick_status_t quick_peer_close(void* ptr);                        /* unmap an imported buffer */
+
+/* Every rank: signal every rank, wait until every rank has reached this barrier (stream-ordered). */
+quick_status_t quick_tp_barrier(void* const* flag_peers, int world, int rank, void* stream);
+
+/* Column-parallel GEMM with the all-gather fused into the epilogue: this rank's
+ * Y_r = X . dequant(Wq_r) (N_local columns, packed = quick_pack_weights of the rank's column shard)
+ * is stored straight into columns [rank N_local, (rank+1) N_local) of EVERY rank's Y (y_peers[p]:
+ * __half [M][ldy], ldy >= world N_local, 16-byte aligned), then a barrier: when the stream passes
+ * this call every rank's Y holds the full [M][world N_local] product.  Same plan, same bits as
+ * quick_w4a16_gemm_ex on the shard.  flags: QUICK_FLAG_PDL / NO_STREAMK; workspace as in _ex.
+ * No rank may still be reading its Y when another rank's call starts writing it (alternate two
+ * Y buffers: each call's closing barrier then makes the reuse two calls later safe). */
+quick_status_t quick_tp_column_gemm(const void* X, const void* packed, int M, int N_local, int K,
+                                    int group_size, void* const* y_peers, int ldy,
+                                    void* const* flag_peers, int world, int rank, int flags,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row-parallel GEMM with a peer-memory all-reduce: the fp32 partial X_local . dequant(Wq_r)
+ * (K_local rows of this rank, N columns) goes to part_peers[rank] (float [M][N], every rank's
+ * mapped here); barrier; this rank sums columns [rank N/P, (rank+1) N/P) over the P partials in
+ * rank order 0..P-1 in fp32 and stores fp16 into every rank's Y (y_peers[p]: __half [M][ldy]);
+ * barrier.  Every rank's Y is bit-identical and deterministic.  N % (8 world) == 0. */
+quick_status_t quick_tp_row_gemm(const void* X_local, const void* packed, int M, int N, int K_local,
+                                 int group_size, void* const* part_peers, void* const* y_peers,
+                                 int ldy, void* const* flag_peers, int world, int rank, int flags,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
 const char* quick_status_string(quick_status_t status);
 
 /* cudaError_t of the last QUICK_ERR_CUDA returned on the calling thread (0 if none). */

@@ -7,7 +7,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libquick.so")
-SOURCES = [os.path.join(CSRC, "quick_gemm.cu"), os.path.join(CSRC, "quick_repack.cu"), os.path.join(CSRC, "quick_pack.cpp")]
+SOURCES = [os.path.join(CSRC, "quick_gemm.cu"), os.path.join(CSRC, "quick_repack.cu"), os.path.join(CSRC, "quick_tp.cu"), os.path.join(CSRC, "quick_pack.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "quick_ptx.cuh"), os.path.join(ROOT, "include", "quick.h")]
 
 NVCC_FLAGS = [
@@ -32,17 +32,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libquick.so next to this file; returns its path."""
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libquick.so next to this file (or `out` with extra -D defines: A/B build variants);
+    returns its path."""
+    target = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES, "-lpthread"]
+    tmp = target + ".tmp"
+    cmd = [nvcc_path(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
+           *SOURCES, "-lpthread"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -91,8 +91,19 @@ struct Cfg {
   // code is written for any power-of-two NPAR.
   static constexpr int NPAR = 2;
   static constexpr int THREADS = 32 * (4 * NPAR + 2);
+  // warp roles: dequant warps 0..4 NPAR - 1, then the producer and the MMA warp.  The build
+  // variant QUICK_ROLES_FIRST puts the producer / MMA warps at ids 0 / 1 instead: measured equal
+  // on B200 over the BJ shapes x M = 1..1024 (tools/gpu_r2_t6.sh, profiles/r02_warp_roles_ab.txt),
+  // and equally imbalanced between the two co-resident stream-K CTAs
+#ifdef QUICK_ROLES_FIRST
+  static constexpr int DQ_BASE = 2;
+  static constexpr int PRODUCER_WARP = 0;
+  static constexpr int MMA_WARP = 1;
+#else
+  static constexpr int DQ_BASE = 0;
   static constexpr int PRODUCER_WARP = 4 * NPAR;
   static constexpr int MMA_WARP = 4 * NPAR + 1;
+#endif
   static constexpr int DQ_THREADS = 128 * NPAR;
   static constexpr int NDBUF = SK ? 2 : 1;
   static constexpr int TMEM_BUDGET = NPAR == 4 ? 512 : 256;
@@ -146,9 +157,16 @@ struct Cfg {
 };
 
 // Kernel parameters (passed by value as a __grid_constant__).
+constexpr int kMaxPeers = 8;   // collective-fused TP epilogue: destinations of every Y store
+
 struct KParams {
   const uint8_t* packed;
   void* Y;
+  // column-parallel TP with the all-gather fused into the epilogue: every Y
+  // element is stored to each of the ndst destinations (this rank's slot of every rank's Y over
+  // peer memory); ndst = 1, Ydst[0] = Y otherwise
+  int ndst;
+  void* Ydst[kMaxPeers];
   int M, N, K, G, g_shift, ldy, flags;
   int n_tiles, m_tiles;   // tile index = t * m_tiles + mt (n-tile major: a CTA's tiles share weights)
   int NA;                 // A stages (128 k) per tile: ceil(K / 128)
@@ -692,8 +710,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     // 1024 + z, -(64 + z)) are rebuilt only when the group changes (G % 128 == 0), or per
     // 32-k chunk otherwise.  Every thread arrives on the barriers itself.  After each segment
     // the same warps run its epilogue (their TMEM lanes, half of the columns each).
-    const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int par = warp >> 2;           // group: A stages a with (a - first) % NPAR == par
+    const int q = warp & 3;              // TMEM lane quarter this warp may access (warp id % 4)
+    const int par = (warp - C::DQ_BASE) >> 2;   // group: A stages a with (a - first) % NPAR == par
     const int r = q * 32 + lane;         // tile row: output column n = 128 t + r
     const uint32_t tlane = (uint32_t)(q * 32) << 16;
     // 32-bit shared-window addresses: explicit ld.shared (a generic pointer through the
@@ -722,7 +740,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       c.s2 = __byte_perm(sbits, 0u, 0x1010);
       return c;
     };
-    const bool tw = TRACE && (warp == 0 && lane == 0);
+    const bool tw = TRACE && (warp == C::DQ_BASE && lane == 0);
     // A stage written: CTA pair members both arrive on the leader's afull (its MMA reads both
     // halves of A from the two TMEMs), one arrival per warp after a warp sync (128 remote
     // per-thread arrivals per stage were measured ~750 cycles slower than local ones)
@@ -894,7 +912,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       const bool silu_store = (lane & 16) == 0;
       ptx::mbar_wait(bar_dfull + 8 * db, (uint32_t)((si >> 1) & 1));
       ptx::tc_fence_after();
-      if (TRACE && tr != nullptr && warp == 0 && lane == 0) tr[1] = clock64();
+      if (TRACE && tr != nullptr && warp == C::DQ_BASE && lane == 0) tr[1] = clock64();
       const uint32_t dcol = tmem + tlane + kDCol + (uint32_t)(db * C::NACC * BN);
       // 8 accumulator columns of this thread's row; with NACC = 2 the two partial sums are
       // added here (fixed order: even K=16 steps + odd K=16 steps)
@@ -931,8 +949,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       };
       // 8 tokens (columns jc .. jc + 7, the first `cnt` valid) of this thread's output column n
       auto store_y8 = [&](int jc, const float (&f)[8], int cnt) {
+#pragma unroll 1
+       for (int d = 0; d < p.ndst; ++d) {
+        void* Yb = p.Ydst[d];
         if (silu) {   // warp-uniform: every lane shuffles, the gate lanes store
-          __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+          __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float u = __shfl_xor_sync(0xffffffffu, f[i], 16);
@@ -941,7 +962,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             asm volatile("" : "+l"(yp));
           }
         } else if (out_fp32) {
-          float* yp = reinterpret_cast<float*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+          float* yp = reinterpret_cast<float*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (i < cnt) *yp = f[i];
@@ -949,7 +970,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             asm volatile("" : "+l"(yp));
           }
         } else {
-          __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+          __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             if (i < cnt) *yp = __float2half_rn(f[i]);
@@ -957,6 +978,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             asm volatile("" : "+l"(yp));
           }
         }
+       }
       };
       const bool whole = SK ? (sg.a_lo == 0 && sg.a_hi == p.NA) : (S == 1);
       const int jmax = min(jend, M - m0);   // valid tokens (columns)
@@ -971,8 +993,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           const int cnt = jmax - jc;   // valid tokens in this chunk (>= 32: all)
           // (the pointer is made opaque after each bump so that the compiler does not keep 32
           // precomputed 64-bit addresses live)
+#pragma unroll 1
+         for (int d = 0; d < p.ndst; ++d) {
+          void* Yb = p.Ydst[d];
           if (silu) {
-            __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+            __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float g = __uint_as_float(v[i]);
@@ -982,7 +1007,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
               asm volatile("" : "+l"(yp));
             }
           } else if (out_fp32) {
-            float* yp = reinterpret_cast<float*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+            float* yp = reinterpret_cast<float*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               if (i < cnt) *yp = __uint_as_float(v[i]);
@@ -990,7 +1015,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
               asm volatile("" : "+l"(yp));
             }
           } else {
-            __half* yp = reinterpret_cast<__half*>(p.Y) + (size_t)(m0 + jc) * p.ldy + n;
+            __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               if (i < cnt) *yp = __float2half_rn(__uint_as_float(v[i]));
@@ -998,6 +1023,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
               asm volatile("" : "+l"(yp));
             }
           }
+         }
         }
       } else if (whole) {
         // the full K range of this tile is in our accumulator: straight to Y
@@ -1054,12 +1080,12 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           }
           ptx::tc_fence_before();
           ptx::mbar_arrive(bar_dempty + 8 * db);   // the accumulator has been read
-          // the named barrier orders every partial store of the CTA before thread 0's gpu-scope
+          // the named barrier orders every partial store of the CTA before one thread's gpu-scope
           // release (cumulativity); nobody waits for the increment itself
           ptx::named_bar_sync(1, kDqThreads);
-          if (threadIdx.x == 0) ptx::red_release_gpu_add(sem, 1);
+          if (threadIdx.x == 32 * C::DQ_BASE) ptx::red_release_gpu_add(sem, 1);   // first dequant thread
         } else {
-          if (threadIdx.x == 0) {
+          if (threadIdx.x == 32 * C::DQ_BASE) {
             const int want = c_last - c_first;
             while (ptx::ld_acquire_gpu(sem) < want) {
             }
@@ -1092,7 +1118,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         ptx::mbar_arrive(bar_dempty + 8 * db);
       }
       ++si;
-      if (TRACE && tr != nullptr && warp == 0 && lane == 0 && whole && !SK) tr[5] = clock64();
+      if (TRACE && tr != nullptr && warp == C::DQ_BASE && lane == 0 && whole && !SK) tr[5] = clock64();
     }
   }
 
@@ -1128,14 +1154,18 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       const int rr = e % kTileRows;
       const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * kTileRows + rr;
       if (out_fp32) {
-        *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Y) + o) = acc;
+#pragma unroll 1
+        for (int d = 0; d < p.ndst; ++d)
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Ydst[d]) + o) = acc;
       } else {
         __half2 lo = __floats2half2_rn(acc.x, acc.y);
         __half2 hi = __floats2half2_rn(acc.z, acc.w);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
+#pragma unroll 1
+        for (int d = 0; d < p.ndst; ++d)
+          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Ydst[d]) + o) = pk;
       }
     };
     // The reduce is latency-bound (a DSMEM load takes ~500 cycles): for S <= 4 each thread keeps
@@ -1189,7 +1219,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         pk.x = *reinterpret_cast<uint32_t*>(&lo);
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
         const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * (kTileRows / 2) + (rr >> 5) * 16 + (rr & 15);
-        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Y) + o) = pk;
+#pragma unroll 1
+        for (int d = 0; d < p.ndst; ++d)
+          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Ydst[d]) + o) = pk;
       }
     } else if (S == 2) {
       reduce_unrolled(std::integral_constant<int, 2>{});
@@ -1893,9 +1925,15 @@ size_t quick_workspace_bytes(int M, int N, int K, int G, int flags, int tile_n, 
   return sk_ws_bytes(tiles, plan.P, plan.tile_n);
 }
 
-quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K, int G,
-                                   void* Y, int ldy, int flags, int tile_n, int split_k,
-                                   void* workspace, size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace quick {
+// The GEMM launch behind quick_w4a16_gemm_ex; `ydst` / `ndst`: every destination of the Y stores
+// (quick_tp.cu's column-parallel GEMM passes one per rank, each a peer-mapped pointer to this
+// rank's column slot of that rank's Y).
+quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int K, int G, void* Y, int ldy,
+                           int flags, int tile_n, int split_k, void* workspace, size_t workspace_bytes,
+                           void* const* ydst, int ndst, void* stream) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
   if (M == 0) return QUICK_OK;
@@ -1938,6 +1976,12 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
 
   kp.packed = static_cast<const uint8_t*>(packed);
   kp.Y = Y;
+  if (ndst < 1 || ndst > kMaxPeers) return QUICK_ERR_INVALID_ARG;
+  kp.ndst = ndst;
+  for (int d = 0; d < ndst; ++d) {
+    if (ydst[d] == nullptr || !aligned(ydst[d], 16)) return QUICK_ERR_INVALID_ARG;
+    kp.Ydst[d] = ydst[d];
+  }
   kp.M = M;
   kp.N = N;
   kp.K = K;
@@ -1977,6 +2021,18 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
     case 128: return launch_bn<128, false>(tmap, kp, s, 0, strm, plan.pair);
     default: return launch_bn<256, false>(tmap, kp, s, 0, strm, plan.pair);
   }
+}
+
+}  // namespace quick
+
+extern "C" {
+
+quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int N, int K, int G,
+                                   void* Y, int ldy, int flags, int tile_n, int split_k,
+                                   void* workspace, size_t workspace_bytes, void* stream) {
+  void* const dst[1] = {Y};
+  return quick::gemm_launch(X, packed, M, N, K, G, Y, ldy, flags, tile_n, split_k, workspace, workspace_bytes,
+                            dst, 1, stream);
 }
 
 quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N, int K, int G,

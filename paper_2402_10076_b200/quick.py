@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libquick.so")
+# QUICK_LIB: an alternative in-tree build of the same library (A/B timing of build variants, tools/)
+LIB_PATH = os.environ.get("QUICK_LIB") or os.path.join(_PKG, "libquick.so")
 
 QUICK_OK, QUICK_ERR_INVALID_ARG, QUICK_ERR_UNSUPPORTED, QUICK_ERR_CUDA = 0, 1, 2, 3
 QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL, QUICK_FLAG_NO_STREAMK, QUICK_FLAG_SILU_MUL = 1, 2, 4, 8
@@ -49,6 +50,16 @@ def _load():
         "quick_dequant_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
         "quick_f32_to_f16": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
         "quick_gather_columns": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
+        "quick_peer_alloc": (c_int, [c_size_t, c_void_p]),
+        "quick_peer_free": (c_int, [c_void_p]),
+        "quick_peer_export": (c_int, [c_void_p, c_void_p]),
+        "quick_peer_import": (c_int, [c_void_p, c_void_p]),
+        "quick_peer_close": (c_int, [c_void_p]),
+        "quick_tp_barrier": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+        "quick_tp_column_gemm": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p,
+                                         c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
+        "quick_tp_row_gemm": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                                      c_void_p, c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
         "quick_status_string": (ctypes.c_char_p, [c_int]),
         "quick_last_cuda_error": (c_int, []),
     }
@@ -319,6 +330,68 @@ def quick_gather_columns(src, P: int, M: int, Nr: int, dst=None, stream=None):
                                                              ctypes.c_void_p(dst.data_ptr()), P, M, Nr,
                                                              _stream_handle(stream)))
     return dst
+
+
+# ----------------------------------------------------------------------------- peer memory / fused TP
+QUICK_IPC_HANDLE_BYTES = 64
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))(*[ctypes.c_void_p(int(p)) for p in ptrs])
+    return arr
+
+
+def quick_peer_alloc(nbytes: int) -> int:
+    p = ctypes.c_void_p()
+    _check("quick_peer_alloc", _lib.quick_peer_alloc(nbytes, ctypes.byref(p)))
+    return int(p.value)
+
+
+def quick_peer_free(ptr: int):
+    _check("quick_peer_free", _lib.quick_peer_free(ctypes.c_void_p(ptr)))
+
+
+def quick_peer_export(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(QUICK_IPC_HANDLE_BYTES)
+    _check("quick_peer_export", _lib.quick_peer_export(ctypes.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def quick_peer_import(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check("quick_peer_import", _lib.quick_peer_import(ctypes.create_string_buffer(handle, len(handle)),
+                                                       ctypes.byref(p)))
+    return int(p.value)
+
+
+def quick_peer_close(ptr: int):
+    _check("quick_peer_close", _lib.quick_peer_close(ctypes.c_void_p(ptr)))
+
+
+def quick_tp_barrier(flag_ptrs, rank: int, stream=None):
+    _check("quick_tp_barrier", _lib.quick_tp_barrier(_ptr_array(flag_ptrs), len(flag_ptrs), rank,
+                                                     _stream_handle(stream)))
+
+
+def quick_tp_column_gemm(x, packed, N_local: int, K: int, group_size: int, y_ptrs, ldy: int, flag_ptrs, rank: int,
+                         *, flags: int = 0, workspace=None, stream=None):
+    """Column-parallel GEMM, all-gather fused into the epilogue (quick.h): y_ptrs / flag_ptrs = every rank's
+    buffer as mapped in this process."""
+    ws_ptr, ws_bytes = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    _check("quick_tp_column_gemm", _lib.quick_tp_column_gemm(
+        ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(packed.data_ptr()), x.shape[0], N_local, K, group_size,
+        _ptr_array(y_ptrs), ldy, _ptr_array(flag_ptrs), len(y_ptrs), rank, flags, ctypes.c_void_p(ws_ptr),
+        ws_bytes, _stream_handle(stream)))
+
+
+def quick_tp_row_gemm(x_local, packed, N: int, K_local: int, group_size: int, part_ptrs, y_ptrs, ldy: int, flag_ptrs,
+                      rank: int, *, flags: int = 0, workspace=None, stream=None):
+    """Row-parallel GEMM + peer-memory fp32 all-reduce (quick.h)."""
+    ws_ptr, ws_bytes = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    _check("quick_tp_row_gemm", _lib.quick_tp_row_gemm(
+        ctypes.c_void_p(x_local.data_ptr()), ctypes.c_void_p(packed.data_ptr()), x_local.shape[0], N, K_local,
+        group_size, _ptr_array(part_ptrs), _ptr_array(y_ptrs), ldy, _ptr_array(flag_ptrs), len(y_ptrs), rank,
+        flags, ctypes.c_void_p(ws_ptr), ws_bytes, _stream_handle(stream)))
 
 
 def quick_status_string(status: int) -> str:

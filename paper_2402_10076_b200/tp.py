@@ -233,3 +233,116 @@ class MegatronAttentionProjections:
     def forward_o(self, attn_r, out=None):
         self.o.workspace = self.workspace
         return self.o.forward(attn_r, out=out)
+
+
+# ----------------------------------------------------------------------------------- fused (peer memory)
+class _DeviceBuffer:
+    """A torch view of a quick_peer_alloc'd buffer (__cuda_array_interface__; no copy)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerComm:
+    """Symmetric peer buffers for the collective-fused TP GEMMs: every rank allocates
+    the same buffers with quick_peer_alloc, exports CUDA IPC handles, and the handles are exchanged
+    over `group` (any torch.distributed backend: plumbing only); each rank then holds every rank's
+    pointer.  One flag array per rank for the barriers (their epochs are counted on the device)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        from . import quick
+        self.quick, self.dist, self.group = quick, dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("at most 8 ranks per node")
+        self._owned, self._imported = [], []
+        self.flags = self.buffer(256)
+
+    def buffer(self, nbytes: int):
+        """Collective: one zeroed device buffer of nbytes per rank; returns every rank's pointer here."""
+        local = self.quick.quick_peer_alloc(nbytes)
+        self._owned.append(local)
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, self.quick.quick_peer_export(local), group=self.group)
+        ptrs = []
+        for p, h in enumerate(handles):
+            if p == self.rank:
+                ptrs.append(local)
+            else:
+                q = self.quick.quick_peer_import(h)
+                self._imported.append(q)
+                ptrs.append(q)
+        return ptrs
+
+    def close(self):
+        import torch
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+        for q in self._imported:
+            self.quick.quick_peer_close(q)
+        self.dist.barrier(group=self.group)
+        for p in self._owned:
+            self.quick.quick_peer_free(p)
+        self._owned, self._imported = [], []
+
+
+class FusedColumnParallelW4A16(ColumnParallelW4A16):
+    """Column-parallel layer whose GEMM epilogue writes this rank's slice into every rank's Y over peer
+    memory (quick_tp_column_gemm): no all-gather call, no gather kernel.  Y alternates between two
+    symmetric buffers (a call's output stays valid until the call after next; the exit barrier of each
+    call makes the reuse safe), so `forward` returns a view of the current one, shape [M][N]."""
+
+    def __init__(self, qweight, scales, zeros, group_size: int, comm: PeerComm, max_tokens: int, device=None):
+        super().__init__(qweight, scales, zeros, group_size, group=comm.group, device=device)
+        self.comm, self.max_tokens = comm, max_tokens
+        nbytes = max_tokens * self.N * 2
+        self._y = [comm.buffer(nbytes), comm.buffer(nbytes)]
+        self._turn = 0
+
+    def forward(self, x, out=None):
+        t = self.torch
+        M = x.shape[0]
+        if M > self.max_tokens:
+            raise ValueError(f"M={M} > max_tokens={self.max_tokens}")
+        ptrs = self._y[self._turn]
+        self._turn ^= 1
+        self.quick.quick_tp_column_gemm(x, self.packed, self.Nr, self.K, self.G, ptrs, self.N, self.comm.flags,
+                                        self.comm.rank, workspace=self.workspace)
+        y = t.as_tensor(_DeviceBuffer(ptrs[self.comm.rank], (M, self.N), "<f2"), device=self.device)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y
+
+
+class FusedRowParallelW4A16(RowParallelW4A16):
+    """Row-parallel layer with the fp32 all-reduce done over peer memory (quick_tp_row_gemm: own fp32
+    partial, each rank reduces 1/P of the columns in rank order and stores fp16 into every rank's Y).
+    Returns a view of the current one of two symmetric Y buffers, shape [M][N]."""
+
+    def __init__(self, qweight, scales, zeros, group_size: int, comm: PeerComm, max_tokens: int, device=None):
+        super().__init__(qweight, scales, zeros, group_size, group=comm.group, device=device)
+        if self.N % (8 * comm.world):
+            raise ValueError("N must be a multiple of 8 x world")
+        self.comm, self.max_tokens = comm, max_tokens
+        self._part = comm.buffer(max_tokens * self.N * 4)
+        self._y = [comm.buffer(max_tokens * self.N * 2), comm.buffer(max_tokens * self.N * 2)]
+        self._turn = 0
+
+    def forward(self, x_shard, out=None):
+        t = self.torch
+        M = x_shard.shape[0]
+        if M > self.max_tokens:
+            raise ValueError(f"M={M} > max_tokens={self.max_tokens}")
+        ptrs = self._y[self._turn]
+        self._turn ^= 1
+        self.quick.quick_tp_row_gemm(x_shard, self.packed, self.N, self.Kr, self.G, self._part, ptrs, self.N,
+                                     self.comm.flags, self.comm.rank, workspace=self.workspace)
+        y = t.as_tensor(_DeviceBuffer(ptrs[self.comm.rank], (M, self.N), "<f2"), device=self.device)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y

@@ -631,3 +631,39 @@ def test_fused_gate_up_silu_mistral_shape(M):
     cols = _cols(I, M, 96)
     res = oracle.tol_check(y.float().cpu().numpy()[:, cols], _silu_ref(pg.x, pg, pu, cols))
     assert res["ok"], res
+
+
+# ------------------------------------------------------------------------------- f3: device repack, GPTQ import
+def _t32(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to(DEV)
+
+
+@pytest.mark.parametrize("K,N,G", [(512, 256, 128), (256, 384, 32), (192, 256, 96), (8192, 28672, 128)])
+def test_device_repack_bit_exact(K, N, G):
+    """quick_pack_weights_device == quick_pack_weights (host C++) == the oracle's v1 encoder (small shapes),
+    byte for byte, incl. the 70B up-projection at full size."""
+    p = synth.make_problem(K * 3 + N, M=1, N=N, K=K, G=G)
+    dev_blob = quick.quick_pack_weights_device(_t32(p.qweight), to_dev_f16(p.scales), _t32(p.zeros), G)
+    torch.cuda.synchronize()
+    host = quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)
+    assert np.array_equal(dev_blob.cpu().numpy(), host)
+    if K * N <= 1 << 20:
+        assert np.array_equal(host, oracle.pack_v1(p.qweight, p.scales, p.zeros, G, K, N))
+
+
+@pytest.mark.parametrize("M,K,N,G,act", [(7, 1024, 512, 128, True), (64, 2048, 256, 64, True), (3, 512, 384, 128, False),
+                                         (200, 1024, 256, 128, True)])
+def test_gptq_import_gemm(M, K, N, G, act):
+    """An AutoGPTQ checkpoint (act-order g_idx, v1 zeros) through quick_import_gptq -> quick_pack_weights ->
+    quick_gather_k(X, perm) -> the GEMM, against the oracle's GPTQ dequant (O8) + GEMM on the original X."""
+    p = synth.make_gptq_problem(M + K + N, M=M, N=N, K=K, G=G, act_order=act)
+    qa, sa, za, perm = quick.quick_import_gptq(p.qweight, p.qzeros, p.scales, G, g_idx=p.g_idx if act else None)
+    blob = torch.from_numpy(quick.quick_pack_weights(qa, sa, za, G)).to(DEV)
+    x = to_dev_f16(p.x)
+    xp = quick.quick_gather_k(x, torch.from_numpy(perm).to(DEV))
+    y = quick.quick_w4a16_gemm(xp, blob, N, K, G, workspace=WS)
+    torch.cuda.synchronize()
+    assert np.array_equal(xp.cpu().numpy().view(np.uint16), p.x[:, perm].view(np.uint16))
+    w = oracle.gptq_dequant(p.qweight, p.qzeros, p.scales, g_idx=p.g_idx if act else None, group_size=G)
+    res = oracle.tol_check(y.float().cpu().numpy(), oracle.gemm(p.x, w))
+    assert res["ok"], res

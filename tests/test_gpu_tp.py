@@ -159,3 +159,64 @@ def test_tp_layers_world2_on_one_gpu():
         pr.join(60)
     want = {"col": True, "row": True, "mlp": True, "attn": True}
     assert out == {0: want, 1: want}, out
+
+
+# ------------------------------------------------------------------------------- f1: collective-fused TP
+def _fused_worker(rank, world, port, q):
+    import traceback
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dev = torch.device("cuda", 0)
+        comm = tp.PeerComm()
+        res = {}
+        # column-parallel: the GEMM epilogue stores into every rank's Y; bit-identical to the collective
+        # path (same per-rank plan) and within tolerance of the oracle; 3 calls (alternating buffers)
+        p = synth.make_problem(71, M=12, N=2048, K=1024, G=128)
+        ref_layer = tp.ColumnParallelW4A16(p.qweight, p.scales, p.zeros, 128, device=dev)
+        fused = tp.FusedColumnParallelW4A16(p.qweight, p.scales, p.zeros, 128, comm, max_tokens=64, device=dev)
+        y_ref = ref_layer.forward(_x(p))
+        ok = True
+        for it in range(3):
+            y = fused.forward(_x(p)).clone()
+            torch.cuda.synchronize()
+            ok &= torch.equal(y.view(torch.int16), y_ref.view(torch.int16))
+        ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+        res["col"] = bool(ok) and oracle.tol_check(y.float().cpu().numpy(), ref)["ok"]
+        # row-parallel: fp32 partials reduced over peer memory in rank order; every rank's Y identical
+        p = synth.make_problem(72, M=9, N=1024, K=4096, G=128)
+        fr = tp.FusedRowParallelW4A16(p.qweight, p.scales, p.zeros, 128, comm, max_tokens=32, device=dev)
+        xs = _x(p)[:, fr.k0:fr.k1].contiguous()
+        outs = [fr.forward(xs).clone() for _ in range(3)]
+        torch.cuda.synchronize()
+        ref = oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128)
+        ok = all(torch.equal(o.view(torch.int16), outs[0].view(torch.int16)) for o in outs)
+        ok &= oracle.tol_check(outs[0].float().cpu().numpy(), ref)["ok"]
+        gathered = [None, None]
+        dist.all_gather_object(gathered, outs[0].cpu().numpy().tobytes())
+        res["row"] = bool(ok) and gathered[0] == gathered[1]
+        comm.close()
+        q.put((rank, res))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_collective_fused_tp_world2_on_one_gpu():
+    """SURVEY §8(f) f1 with two ranks sharing cuda:0 through CUDA IPC: the column-parallel epilogue writes
+    straight into both ranks' Y, the row-parallel partials are reduced over peer memory."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for pr in procs:
+        pr.join(60)
+    assert out == {0: {"col": True, "row": True}, 1: {"col": True, "row": True}}, out

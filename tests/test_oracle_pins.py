@@ -345,3 +345,59 @@ def test_silu_mul_against_torch():
     g, u = rng.normal(0, 4, 1000), rng.normal(0, 1, 1000)
     ref = (torch.nn.functional.silu(torch.from_numpy(g)) * torch.from_numpy(u)).numpy()
     np.testing.assert_allclose(oracle.silu_mul(g, u), ref, rtol=1e-13, atol=1e-300)
+
+
+# ------------------------------------------------------------------ O8 gptq_dequant (R17)
+def test_gptq_dequant_hand_example():
+    """Hand-computed: one column block, rows 0..7 hold codes 1..8 (word 0x87654321, nibble i = row i),
+    stored zero 7 in a v1 checkpoint (decoded zero 8), scale 0.5: w[k] = (k + 1 - 8) * 0.5."""
+    K, N, G = 8, 8, 8
+    qweight = np.full((K // 8, N), 0x87654321, dtype=np.uint32)
+    qzeros = np.array([[0x77777777]], dtype=np.uint32)
+    scales = np.full((1, N), 0.5, dtype=np.float16)
+    w = oracle.gptq_dequant(qweight, qzeros, scales, group_size=G)
+    expect = np.array([-3.5, -3.0, -2.5, -2.0, -1.5, -1.0, -0.5, 0.0])
+    for n in range(N):
+        assert w[:, n].astype(np.float64).tolist() == expect.tolist()
+    # "v2" (zeros stored as is): decoded zero 7
+    w2 = oracle.gptq_dequant(qweight, qzeros, scales, group_size=G, zero_plus_one=False)
+    assert w2[:, 0].astype(np.float64).tolist() == (expect + 0.5).tolist()
+
+
+def test_gptq_packing_order_matches_vllm():
+    """vLLM's gptq_pack (pack_rows: 8 rows per word) and pack_cols (8 columns per word, natural order)
+    are the library statement of the AutoGPTQ layout: with unit scales and zero 0 (v2) the oracle
+    returns the packed codes; with act-order g_idx each row takes its own group's zero and scale."""
+    torch = pytest.importorskip("torch")
+    qu = pytest.importorskip("vllm.model_executor.layers.quantization.utils.quant_utils")
+    rng = np.random.default_rng(11)
+    K, N, G = 64, 32, 16
+    codes = rng.integers(0, 16, (K, N))
+    qweight = qu.pack_rows(torch.from_numpy(codes), 4, K, N).numpy().view(np.uint32)
+    zeros = rng.integers(0, 16, (K // G, N))
+    qzeros = qu.pack_cols(torch.from_numpy(zeros), 4, K // G, N).numpy().view(np.uint32)
+    ones = np.ones((K // G, N), np.float16)
+    w = oracle.gptq_dequant(qweight, np.zeros_like(qzeros), ones, group_size=G, zero_plus_one=False)
+    assert np.array_equal(w.astype(np.int64), codes)
+    g_idx = rng.permutation(np.arange(K) // G)
+    scales = (rng.integers(1, 64, (K // G, N)) / 64).astype(np.float16)
+    w = oracle.gptq_dequant(qweight, qzeros, scales, g_idx=g_idx, zero_plus_one=False)
+    ref = ((codes - zeros[g_idx]) * scales.astype(np.float64)[g_idx]).astype(np.float16)   # exact products
+    assert np.array_equal(w.view(np.uint16), ref.view(np.uint16))
+
+
+def test_gptq_v2_without_act_order_is_the_awq_dequant():
+    """Same codes, zeros and scales written in the two checkpoint layouts: O8 (GPTQ, v2 zeros) equals
+    O2 (AWQ), whose packing order is pinned against vLLM's awq_pack above."""
+    p = synth.make_problem(17, M=1, N=64, K=128, G=32)
+    codes = oracle.unpack_awq(p.qweight)
+    zeros = oracle.unpack_awq(p.zeros)
+    qweight = np.zeros((128 // 8, 64), np.uint32)
+    for i in range(8):
+        qweight |= (codes[i::8, :].astype(np.uint32) << np.uint32(4 * i))
+    qzeros = np.zeros((4, 8), np.uint32)
+    for i in range(8):
+        qzeros |= (zeros[:, i::8].astype(np.uint32) << np.uint32(4 * i))
+    w_gptq = oracle.gptq_dequant(qweight, qzeros, p.scales, group_size=32, zero_plus_one=False)
+    w_awq = oracle.dequant(p.qweight, p.scales, p.zeros, 32)
+    assert np.array_equal(w_gptq.view(np.uint16), w_awq.view(np.uint16))

@@ -114,3 +114,33 @@ def test_pack_gate_up_rejects_bad_shapes():
     pg = synth.make_problem(1, M=1, N=64, K=128, G=64)
     with pytest.raises(ValueError):
         quick.quick_pack_gate_up((pg.qweight, pg.scales, pg.zeros), (pu.qweight, pu.scales, pu.zeros), 64)
+
+
+# ------------------------------------------------------------------ GPTQ import (f3)
+@pytest.mark.parametrize("K,N,G,act", [(256, 128, 64, True), (512, 256, 128, True), (256, 128, 32, False)])
+def test_import_gptq_reorders_rows_by_group(K, N, G, act):
+    """quick_import_gptq: the imported AWQ tensors dequantize (oracle O2) to the GPTQ weights (oracle O8)
+    with the rows in the order perm, bit for bit; perm sorts the rows by group."""
+    p = synth.make_gptq_problem(K + N, M=1, N=N, K=K, G=G, act_order=act)
+    qa, sa, za, perm = quick.quick_import_gptq(p.qweight, p.qzeros, p.scales, G, g_idx=p.g_idx if act else None)
+    w_gptq = oracle.gptq_dequant(p.qweight, p.qzeros, p.scales, g_idx=p.g_idx if act else None, group_size=G)
+    w_imp = oracle.dequant(qa, sa, za, G)
+    assert np.array_equal(w_imp.view(np.uint16), w_gptq[perm].view(np.uint16))
+    assert np.array_equal(np.sort(perm), np.arange(K))
+    gi = p.g_idx if act else np.arange(K) // G
+    assert np.array_equal(gi[perm], np.arange(K) // G)
+    if not act:
+        assert np.array_equal(perm, np.arange(K))
+
+
+def test_import_gptq_rejects_unrepresentable_zero_and_ragged_groups():
+    p = synth.make_gptq_problem(3, M=1, N=128, K=256, G=64)
+    bad = p.qzeros.copy()
+    bad[0, 0] |= np.uint32(0xF)            # stored 15 -> decoded zero 16 in a v1 checkpoint
+    with pytest.raises(quick.QuickError):
+        quick.quick_import_gptq(p.qweight, bad, p.scales, 64, g_idx=p.g_idx)
+    quick.quick_import_gptq(p.qweight, bad, p.scales, 64, g_idx=p.g_idx, zero_plus_one=False)   # v2: zero 15
+    g = p.g_idx.copy()
+    g[0] = (g[0] + 1) % 4                  # one group with G + 1 rows, another with G - 1
+    with pytest.raises(quick.QuickError):
+        quick.quick_import_gptq(p.qweight, p.qzeros, p.scales, 64, g_idx=g)
