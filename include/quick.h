@@ -109,6 +109,10 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
                                 also dequantized before that point.  Ignored by plans with
                                 256-token tiles. */
 #define QUICK_FLAG_NO_STREAMK 4 /* never use the stream-K schedule (tests / A-B timing) */
+#define QUICK_FLAG_BF16 16      /* bf16 variant: X, Y and the blob's 16-bit
+                                   scales are bf16 (quick_pack_weights copies the scale bits as
+                                   given); dequant = bf16_rne((q - z) * s), fp32 accumulation, bf16
+                                   Y (or fp32 with QUICK_FLAG_OUT_F32). */
 #define QUICK_FLAG_SILU_MUL 8   /* fused gate||up epilogue for a blob made by
                                    quick_pack_gate_up: Y is __half [M][N/2] (ldy >= N/2) with
                                    Y[m][i] = fp16_rne(SiLU(G[m][i]) * U[m][i]), G = X.gate and
@@ -169,6 +173,10 @@ quick_status_t quick_gather_k(const void* X, const int32_t* perm, int M, int K, 
  * dequant(q)[k][n] bit-exactly as fp16_rne((q - z) * s) (§2.3).  Asynchronous. */
 quick_status_t quick_dequant_weights(const void* packed, int K, int N, int group_size, void* W,
                                      void* stream);
+
+/* quick_dequant_weights with flags: QUICK_FLAG_BF16 -> bf16_rne((q - z) * s), W bf16 [K][N]. */
+quick_status_t quick_dequant_weights_ex(const void* packed, int K, int N, int group_size, void* W,
+                                        int flags, void* stream);
 
 /* Row-parallel epilogue: dst[i] = fp16_rne(src[i]) for i < n (device float -> device __half). */
 quick_status_t quick_f32_to_f16(const void* src, void* dst, size_t n, void* stream);

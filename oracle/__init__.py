@@ -20,6 +20,11 @@ from .quick_oracle import (  # noqa: F401
     round_fp16,
     silu_mul,
     gptq_dequant,
+    bf16_rne,
+    bf16_bits,
+    bf16_from_bits,
+    dequant_bf16,
+    gemm_f64,
     tol_check,
     v1_packed_bytes,
     v1_weight_pos,

@@ -22,6 +22,11 @@ What the path computes (PAPER.md = /root/reference/PAPER.md, "P:L<n>" = its line
               form of §3.2): an independent encoder/decoder written from the layout
               text, used to check the library packer bit-for-bit.
 
+  O9 bf16     (the bf16 variant; R18): bf16 activations, scales and
+              output.  bf16_rne rounds to 8 significant bits (round half to even, exponent range
+              of fp32); dequant w = bf16_rne((q - z) * s) (the product is exact in fp64); the GEMM
+              sums exact products in fp64 like O3; bf16 values are carried as float64 arrays and
+              as uint16 bit patterns (numpy has no bf16 dtype).
   O8 gptq     (GPTQ is the P:L19 family): dequantization of an AutoGPTQ
               checkpoint, w[k][n] = fp16_rne((q[k][n] - z[g_idx[k]][n]) * s[g_idx[k]][n]),
               q packed 8 rows per word (nibble i = row 8j + i), z packed 8 columns per word
@@ -93,6 +98,40 @@ def gemm(x: np.ndarray, w: np.ndarray) -> np.ndarray:
 def w4a16_reference(x, qweight, scales, zeros, group_size) -> np.ndarray:
     """O1 -> O2 -> O3: the fp64 reference of Y = X . dequant(Wq)."""
     return gemm(x, dequant(qweight, scales, zeros, group_size))
+
+
+# ----------------------------------------------------------------------------------------- O9
+def bf16_rne(x) -> np.ndarray:
+    """O9: round float64 values to bf16 (8 significant bits, nearest, ties to even), returned as
+    float64.  Finite inputs well inside the fp32 exponent range (the path's values) only."""
+    x = np.asarray(x, dtype=np.float64)
+    m, e = np.frexp(x)                              # x = m 2^e, 0.5 <= |m| < 1
+    r = np.rint(np.ldexp(m, 8))                     # 8 significant bits; np.rint ties to even
+    return np.ldexp(r, e - 8)
+
+
+def bf16_bits(x) -> np.ndarray:
+    """uint16 bit patterns of bf16-representable float64 values (the upper half of their fp32 bits)."""
+    f = np.asarray(x, dtype=np.float64).astype(np.float32)
+    return (f.view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def bf16_from_bits(bits) -> np.ndarray:
+    return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def dequant_bf16(qweight, scale_bits, zeros, group_size) -> np.ndarray:
+    """O9: w[k][n] = bf16_rne((q - z) * s) with s given as bf16 bits [K/G][N]; float64 [K][N]."""
+    q = unpack_awq(qweight).astype(np.int64)
+    z = unpack_awq(zeros).astype(np.int64)
+    s = bf16_from_bits(scale_bits)
+    g = np.arange(q.shape[0]) // group_size
+    return bf16_rne((q - z[g, :]).astype(np.float64) * s[g, :])
+
+
+def gemm_f64(x: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """O9's O3: Y = X . W for operands already exact in float64 (bf16 values), fp64 accumulation."""
+    return np.asarray(x, dtype=np.float64) @ np.asarray(w, dtype=np.float64)
 
 
 # ----------------------------------------------------------------------------------------- O8

@@ -25,6 +25,7 @@
 // Split-K: the S CTAs of a (S,1,1) cluster share one (n-tile, m-tile) and split K (the
 // "split-k" knob of §5); partial sums stay fp32 (tolerance analysis).
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -302,6 +303,62 @@ __device__ __forceinline__ void dequant_word(uint32_t w, const DequantConsts& c,
   out[3] = hmul2_rn(hfma2_rn(hi1, kInv16, c.zhi), c.s2);
 }
 
+// bf16 variant (QUICK_FLAG_BF16): X, scales and Y in bf16.  bf16 has an 8-bit
+// significand, so the magic number is 128 (0x4300, ulp 1 up to 256): each nibble pair is shifted to
+// bits 0-3 / 16-19 and OR-ed into 0x4300 4300 -> bf16 (128 + q); (q - z) = that - (128 + z), exact;
+// one bf16 RN multiply by s -> bf16_rne((q - z) * s), bit-identical to the oracle's bf16 dequant.
+// Output pairs (k0,k1), (k2,k3), (k4,k5), (k6,k7) as for fp16 (same v1 nibble order).
+__device__ __forceinline__ uint32_t bsub2_rn(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t bmul2_rn(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ void dequant_word_bf16(uint32_t w, const DequantConsts& c, uint32_t* out) {
+  constexpr uint32_t kMagic = 0x43004300u;   // bf16x2 (128, 128)
+  out[0] = bmul2_rn(bsub2_rn(ptx::lop3<0xEA>(w, 0x000F000Fu, kMagic), c.zlo), c.s2);
+  out[1] = bmul2_rn(bsub2_rn(ptx::lop3<0xEA>(w >> 4, 0x000F000Fu, kMagic), c.zlo), c.s2);
+  out[2] = bmul2_rn(bsub2_rn(ptx::lop3<0xEA>(w >> 8, 0x000F000Fu, kMagic), c.zlo), c.s2);
+  out[3] = bmul2_rn(bsub2_rn(ptx::lop3<0xEA>(w >> 12, 0x000F000Fu, kMagic), c.zlo), c.s2);
+}
+template <bool BF>
+__device__ __forceinline__ void dequant_w(uint32_t w, const DequantConsts& c, uint32_t* out) {
+  if constexpr (BF)
+    dequant_word_bf16(w, c, out);
+  else
+    dequant_word(w, c, out);
+}
+// group constants of the bf16 variant: zlo = bf16x2 (128 + z), s2 = (s, s)
+__device__ __forceinline__ DequantConsts make_consts_bf16(uint32_t sbits, uint32_t z) {
+  DequantConsts c;
+  c.zlo = __byte_perm(0x4300u + z, 0u, 0x1010);
+  c.zhi = 0u;
+  c.s2 = __byte_perm(sbits, 0u, 0x1010);
+  return c;
+}
+// 16-bit output conversions (fp16 or bf16, round to nearest even)
+template <bool BF>
+__device__ __forceinline__ uint16_t cvt16(float f) {
+  if constexpr (BF)
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+  else
+    return __half_as_ushort(__float2half_rn(f));
+}
+template <bool BF>
+__device__ __forceinline__ uint32_t cvt16x2(float a, float b) {
+  if constexpr (BF) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
 // SiLU(g) * u in fp32 (the fused gate||up epilogue, QUICK_FLAG_SILU_MUL)
 __device__ __forceinline__ float silu_mul(float g, float u) {
   return g * __frcp_rn(1.0f + __expf(-g)) * u;
@@ -320,12 +377,13 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
 
 // tcgen05 instruction descriptor, kind::f16: D fp32, A/B fp16, both K-major, M=128 (256 for a
 // CTA pair), N=BN
-template <int BN, int MM = kTileRows>
+template <int BN, int MM = kTileRows, bool BF = false>
 __device__ __forceinline__ constexpr uint32_t instr_desc() {
-  return (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
+  // bits 7-9 / 10-12: A / B format of kind::f16 (0 = fp16, 1 = bf16)
+  return (1u << 4) | (BF ? (1u << 7) | (1u << 10) : 0u) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(MM >> 4) << 24);
 }
 
-template <int BN, bool SK, bool GBIG, bool TRACE, int AM = 0>
+template <int BN, bool SK, bool GBIG, bool TRACE, int AM = 0, bool BF = false>
 __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX_CTAS_PER_SM)
     quick_w4a16_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                           const __grid_constant__ KParams p) {
@@ -529,7 +587,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     // ------------------------------------------------------------------ MMA issuer
     // Warp-uniform loop; one elected lane issues the MMAs and the commits (a commit tracks
     // the async tcgen05 ops of the thread that issues it, so the same lane does both).
-    constexpr uint32_t idesc = instr_desc<BN, PAIR ? 2 * kTileRows : kTileRows>();
+    constexpr uint32_t idesc = instr_desc<BN, PAIR ? 2 * kTileRows : kTileRows, BF>();
     const uint64_t desc0 = sw128_desc(sbase + C::X_OFF);
     // AM = 1: the A stage is an SW128 K-major tile in shared memory (two 64-k sub-tiles of 16 KiB)
     const uint64_t adesc0 = sw128_desc(sbase + (uint32_t)C::A_OFF);
@@ -735,8 +793,13 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       const uint32_t sbits = ptx::lds_u16(mrow + mo);
       const uint32_t zr = __byte_perm(zb, 0u, 0x4040);   // [zb, 0, zb, 0]
       DequantConsts c;
-      c.zlo = ptx::lop3<0xEA>(zr >> zsh, 0x000F000Fu, 0x64006400u);
-      c.zhi = ptx::lop3<0xEA>(zr << zsh_hi, 0x00F000F0u, 0xD400D400u);
+      if constexpr (BF) {
+        c.zlo = ptx::lop3<0xEA>(zr >> zsh, 0x000F000Fu, 0x43004300u);   // bf16 (128 + z)
+        c.zhi = 0u;
+      } else {
+        c.zlo = ptx::lop3<0xEA>(zr >> zsh, 0x000F000Fu, 0x64006400u);
+        c.zhi = ptx::lop3<0xEA>(zr << zsh_hi, 0x00F000F0u, 0xD400D400u);
+      }
       c.s2 = __byte_perm(sbits, 0u, 0x1010);
       return c;
     };
@@ -818,15 +881,15 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
             arrive_afull(as);
           } else {
-            dequant_word(w[0].x, cst, a_regs + 0);
-            dequant_word(w[0].y, cst, a_regs + 4);
-            dequant_word(w[0].z, cst, a_regs + 8);
-            dequant_word(w[0].w, cst, a_regs + 12);
+            dequant_w<BF>(w[0].x, cst, a_regs + 0);
+            dequant_w<BF>(w[0].y, cst, a_regs + 4);
+            dequant_w<BF>(w[0].z, cst, a_regs + 8);
+            dequant_w<BF>(w[0].w, cst, a_regs + 12);
             const DequantConsts& c1 = GBIG ? cst : cst1;
-            dequant_word(w[1].x, c1, a_regs + 16);
-            dequant_word(w[1].y, c1, a_regs + 20);
-            dequant_word(w[1].z, c1, a_regs + 24);
-            dequant_word(w[1].w, c1, a_regs + 28);
+            dequant_w<BF>(w[1].x, c1, a_regs + 16);
+            dequant_w<BF>(w[1].y, c1, a_regs + 20);
+            dequant_w<BF>(w[1].z, c1, a_regs + 24);
+            dequant_w<BF>(w[1].w, c1, a_regs + 28);
             ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
             if (tw) stamp(3, iw);
             ptx::tc_fence_after();
@@ -856,14 +919,14 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
               const DequantConsts& c2 = GBIG ? cst : cst2;
               const DequantConsts& c3 = GBIG ? cst : cst3;
               uint32_t b_regs[32];
-              dequant_word(w[2].x, c2, b_regs + 0);
-              dequant_word(w[2].y, c2, b_regs + 4);
-              dequant_word(w[2].z, c2, b_regs + 8);
-              dequant_word(w[2].w, c2, b_regs + 12);
-              dequant_word(w[3].x, c3, b_regs + 16);
-              dequant_word(w[3].y, c3, b_regs + 20);
-              dequant_word(w[3].z, c3, b_regs + 24);
-              dequant_word(w[3].w, c3, b_regs + 28);
+              dequant_w<BF>(w[2].x, c2, b_regs + 0);
+              dequant_w<BF>(w[2].y, c2, b_regs + 4);
+              dequant_w<BF>(w[2].z, c2, b_regs + 8);
+              dequant_w<BF>(w[2].w, c2, b_regs + 12);
+              dequant_w<BF>(w[3].x, c3, b_regs + 16);
+              dequant_w<BF>(w[3].y, c3, b_regs + 20);
+              dequant_w<BF>(w[3].z, c3, b_regs + 24);
+              dequant_w<BF>(w[3].w, c3, b_regs + 28);
               if (dbg_nosttm) {
                 uint32_t x = 0;
 #pragma unroll
@@ -953,11 +1016,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
        for (int d = 0; d < p.ndst; ++d) {
         void* Yb = p.Ydst[d];
         if (silu) {   // warp-uniform: every lane shuffles, the gate lanes store
-          __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
+          uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float u = __shfl_xor_sync(0xffffffffu, f[i], 16);
-            if (i < cnt && silu_store) *yp = __float2half_rn(silu_mul(f[i], u));
+            if (i < cnt && silu_store) *yp = cvt16<BF>(silu_mul(f[i], u));
             yp += p.ldy;
             asm volatile("" : "+l"(yp));
           }
@@ -970,10 +1033,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             asm volatile("" : "+l"(yp));
           }
         } else {
-          __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
+          uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (i < cnt) *yp = __float2half_rn(f[i]);
+            if (i < cnt) *yp = cvt16<BF>(f[i]);
             yp += p.ldy;
             asm volatile("" : "+l"(yp));
           }
@@ -997,12 +1060,12 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
          for (int d = 0; d < p.ndst; ++d) {
           void* Yb = p.Ydst[d];
           if (silu) {
-            __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
+            uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float g = __uint_as_float(v[i]);
               const float u = __shfl_xor_sync(0xffffffffu, g, 16);
-              if (i < cnt && silu_store) *yp = __float2half_rn(silu_mul(g, u));
+              if (i < cnt && silu_store) *yp = cvt16<BF>(silu_mul(g, u));
               yp += p.ldy;
               asm volatile("" : "+l"(yp));
             }
@@ -1015,10 +1078,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
               asm volatile("" : "+l"(yp));
             }
           } else {
-            __half* yp = reinterpret_cast<__half*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
+            uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              if (i < cnt) *yp = __float2half_rn(__uint_as_float(v[i]));
+              if (i < cnt) *yp = cvt16<BF>(__uint_as_float(v[i]));
               yp += p.ldy;
               asm volatile("" : "+l"(yp));
             }
@@ -1158,14 +1221,12 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         for (int d = 0; d < p.ndst; ++d)
           *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.Ydst[d]) + o) = acc;
       } else {
-        __half2 lo = __floats2half2_rn(acc.x, acc.y);
-        __half2 hi = __floats2half2_rn(acc.z, acc.w);
         uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        pk.x = cvt16x2<BF>(acc.x, acc.y);
+        pk.y = cvt16x2<BF>(acc.z, acc.w);
 #pragma unroll 1
         for (int d = 0; d < p.ndst; ++d)
-          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Ydst[d]) + o) = pk;
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.Ydst[d]) + o) = pk;
       }
     };
     // The reduce is latency-bound (a DSMEM load takes ~500 cycles): for S <= 4 each thread keeps
@@ -1213,15 +1274,13 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           g.x += g2.x; g.y += g2.y; g.z += g2.z; g.w += g2.w;
           u.x += u2.x; u.y += u2.y; u.z += u2.z; u.w += u2.w;
         }
-        __half2 lo = __floats2half2_rn(silu_mul(g.x, u.x), silu_mul(g.y, u.y));
-        __half2 hi = __floats2half2_rn(silu_mul(g.z, u.z), silu_mul(g.w, u.w));
         uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&lo);
-        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        pk.x = cvt16x2<BF>(silu_mul(g.x, u.x), silu_mul(g.y, u.y));
+        pk.y = cvt16x2<BF>(silu_mul(g.z, u.z), silu_mul(g.w, u.w));
         const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * (kTileRows / 2) + (rr >> 5) * 16 + (rr & 15);
 #pragma unroll 1
         for (int d = 0; d < p.ndst; ++d)
-          *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(p.Ydst[d]) + o) = pk;
+          *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(p.Ydst[d]) + o) = pk;
       }
     } else if (S == 2) {
       reduce_unrolled(std::integral_constant<int, 2>{});
@@ -1301,7 +1360,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 // Utility kernels on the same layout.
 // ------------------------------------------------------------------------------------------
 // One thread per 16-byte chunk (t, c, r): 32 codes of column n = 128t + r, k = 32c..32c+31.
-__global__ void quick_dequant_kernel(const uint8_t* __restrict__ packed, __half* __restrict__ W,
+template <bool BF>
+__global__ void quick_dequant_kernel(const uint8_t* __restrict__ packed, uint16_t* __restrict__ W,
                                      int K, int N, int G) {
   const int C32 = K / 32;
   const long long total = (long long)(N / kTileRows) * C32 * kTileRows;
@@ -1315,14 +1375,14 @@ __global__ void quick_dequant_kernel(const uint8_t* __restrict__ packed, __half*
   const uint8_t* meta = packed + (size_t)K * N / 2 + ((size_t)t * (K / G) + g) * kMetaBytes;
   const uint32_t sbits = reinterpret_cast<const uint16_t*>(meta)[r];
   const uint32_t z = (meta[256 + (r >> 1)] >> ((r & 1) * 4)) & 0xFu;
-  const DequantConsts dc = make_consts(sbits, z);
+  const DequantConsts dc = BF ? make_consts_bf16(sbits, z) : make_consts(sbits, z);
   uint32_t a[16];
-  dequant_word(wv.x, dc, a + 0);
-  dequant_word(wv.y, dc, a + 4);
-  dequant_word(wv.z, dc, a + 8);
-  dequant_word(wv.w, dc, a + 12);
+  dequant_w<BF>(wv.x, dc, a + 0);
+  dequant_w<BF>(wv.y, dc, a + 4);
+  dequant_w<BF>(wv.z, dc, a + 8);
+  dequant_w<BF>(wv.w, dc, a + 12);
   const int n = t * kTileRows + r;
-  uint16_t* Wb = reinterpret_cast<uint16_t*>(W);
+  uint16_t* Wb = W;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const size_t k = (size_t)32 * c + 2 * i;
@@ -1443,6 +1503,21 @@ void* kernel_for_t(int bn, bool sk, bool gbig) {
   }
 }
 void* kernel_for(int bn, bool sk, bool gbig = true) { return kernel_for_t<false>(bn, sk, gbig); }
+// the bf16 variant (QUICK_FLAG_BF16): no trace instantiation
+template <int BN, bool SK>
+void* bf16_ptr2(bool gbig) {
+  return gbig ? reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, SK, true, false, 0, true>)
+              : reinterpret_cast<void*>(quick::quick_w4a16_tc_kernel<BN, SK, false, false, 0, true>);
+}
+void* bf16_kernel_for(int bn, bool sk, bool gbig) {
+  switch (bn) {
+    case 16: return sk ? bf16_ptr2<16, true>(gbig) : bf16_ptr2<16, false>(gbig);
+    case 32: return sk ? bf16_ptr2<32, true>(gbig) : bf16_ptr2<32, false>(gbig);
+    case 64: return sk ? bf16_ptr2<64, true>(gbig) : bf16_ptr2<64, false>(gbig);
+    case 128: return bf16_ptr2<128, false>(gbig);
+    default: return bf16_ptr2<256, false>(gbig);
+  }
+}
 void* trace_kernel_for(int bn, bool sk, bool gbig = true) { return kernel_for_t<true>(bn, sk, gbig); }
 
 #define QUICK_CFG_FIELD(FN, FIELD)                                                        \
@@ -1471,8 +1546,8 @@ cudaError_t configure_kernel(int bn, bool sk) {
   cudaError_t e = cudaSuccess;
   // every (group-size specialisation, trace) variant; the whole unified L1/shared array as
   // shared memory: two 80-110 KiB CTAs per SM
-  for (int v = 0; v < 4 && e == cudaSuccess; ++v) {
-    void* k = (v & 2) ? trace_kernel_for(bn, sk, v & 1) : kernel_for(bn, sk, v & 1);
+  for (int v = 0; v < 6 && e == cudaSuccess; ++v) {
+    void* k = v >= 4 ? bf16_kernel_for(bn, sk, v & 1) : (v & 2) ? trace_kernel_for(bn, sk, v & 1) : kernel_for(bn, sk, v & 1);
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              std::max(smem_for(bn, sk), 120 * 1024));   // 120 KiB: kDebugOneCta
     if (e == cudaSuccess)
@@ -1758,10 +1833,13 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   // group-size specialisation: a power of two >= 128 (the group index is a shift and an A
   // stage never straddles groups); any other G takes the per-32-k general path
   const bool gbig = kp.G >= quick::kKA && (kp.G & (kp.G - 1)) == 0;
+  const bool bf = (kp.flags & QUICK_FLAG_BF16) != 0;
   if constexpr (!SK && BN >= 128) {
     if (pair) {   // CTA pairs (cta_group::2): grid (2 S, n_tiles / 2, m_tiles), clusters of 2 S
       using CP = quick::Cfg<BN, false, 2>;
-      auto* kq = g_trace != nullptr ? (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, true, 2>
+      auto* kq = bf ? (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, false, 2, true>
+                            : quick::quick_w4a16_tc_kernel<BN, false, false, false, 2, true>)
+               : g_trace != nullptr ? (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, true, 2>
                                             : quick::quick_w4a16_tc_kernel<BN, false, false, true, 2>)
                                     : (gbig ? quick::quick_w4a16_tc_kernel<BN, false, true, false, 2>
                                             : quick::quick_w4a16_tc_kernel<BN, false, false, false, 2>);
@@ -1801,7 +1879,10 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
       return QUICK_OK;
     }
   }
-  if (g_trace != nullptr)
+  if (bf)
+    e = gbig ? cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true, false, 0, true>, tmap, kp)
+             : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, false, 0, true>, tmap, kp);
+  else if (g_trace != nullptr)
     e = gbig ? cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, true, true>, tmap, kp)
              : cudaLaunchKernelEx(&cfg, quick::quick_w4a16_tc_kernel<BN, SK, false, true>, tmap, kp);
   else
@@ -1812,6 +1893,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
 }
 
 constexpr int kKnownFlags = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_STREAMK | QUICK_FLAG_SILU_MUL |
+                            QUICK_FLAG_BF16 |
                             quick::kDebugNoCompute |
                             quick::kDebugExitTop | quick::kDebugExitPrologue | quick::kDebugNoMma |
                             quick::kDebugOneCta | quick::kDebugNoSttm | quick::kDebugPdlEarly |
@@ -1833,10 +1915,11 @@ Plan plan_for(int M, int N, int K, int G, int flags, int tile_n, int split_k, bo
 // TMA descriptor of X viewed as [K/64][M][64], box {64, rows, kc}.  Encoding costs host
 // microseconds, so descriptors are cached per thread, keyed by everything they encode (the
 // pointer, M, K and the box): a hit is always the same descriptor the encoder would produce.
-bool x_tensor_map(const void* X, int M, int K, int rows, int kc, CUtensorMap* out) {
+bool x_tensor_map(const void* X, int M, int K, int rows, int kc, bool bf, CUtensorMap* out) {
   struct Entry {
     const void* x;
     int M, K, rows, kc;
+    bool bf;
     CUtensorMap map;
   };
   constexpr int kEntries = 32;
@@ -1844,7 +1927,7 @@ bool x_tensor_map(const void* X, int M, int K, int rows, int kc, CUtensorMap* ou
   thread_local int used = 0, next = 0;
   for (int i = 0; i < used; ++i) {
     const Entry& e = cache[i];
-    if (e.x == X && e.M == M && e.K == K && e.rows == rows && e.kc == kc) {
+    if (e.x == X && e.M == M && e.K == K && e.rows == rows && e.kc == kc && e.bf == bf) {
       *out = e.map;
       return true;
     }
@@ -1855,12 +1938,13 @@ bool x_tensor_map(const void* X, int M, int K, int rows, int kc, CUtensorMap* ou
   cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
   cuuint32_t box[3] = {64, (cuuint32_t)rows, (cuuint32_t)kc};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(X), dims, strides, box, estr,
+  CUresult cr = enc(out, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                    const_cast<void*>(X), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return false;
   Entry& e = cache[next];
-  e = Entry{X, M, K, rows, kc, *out};
+  e = Entry{X, M, K, rows, kc, bf, *out};
   next = (next + 1) % kEntries;
   if (used < kEntries) ++used;
   return true;
@@ -1943,6 +2027,7 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   if (ldy < (silu ? N / 2 : N)) return QUICK_ERR_INVALID_ARG;
   if (ldy % 8 != 0 || (flags & ~kKnownFlags) != 0) return QUICK_ERR_UNSUPPORTED;
   if (silu && (flags & (QUICK_FLAG_OUT_F32 | quick::kAblationSmemA))) return QUICK_ERR_UNSUPPORTED;
+  if ((flags & QUICK_FLAG_BF16) && (flags & quick::kAblationSmemA)) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (workspace_bytes != 0 && (workspace == nullptr || !aligned(workspace, 256))) return QUICK_ERR_INVALID_ARG;
   if (tile_n != 0 && tile_index(tile_n) < 0) return QUICK_ERR_UNSUPPORTED;
@@ -1972,7 +2057,8 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   // 3-D box {64, tile_n, KL/64} lands as KL/64 SWIZZLE_128B [tile_n][64] sub-tiles.
   CUtensorMap tmap;
   const int kl = kl_for(tn, plan.sk);
-  if (!x_tensor_map(X, M, K, plan.pair ? tn / 2 : tn, kl / 64, &tmap)) return cuda_fail(cudaErrorInvalidValue);
+  if (!x_tensor_map(X, M, K, plan.pair ? tn / 2 : tn, kl / 64, (flags & QUICK_FLAG_BF16) != 0, &tmap))
+    return cuda_fail(cudaErrorInvalidValue);
 
   kp.packed = static_cast<const uint8_t*>(packed);
   kp.Y = Y;
@@ -2042,6 +2128,12 @@ quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N,
 
 quick_status_t quick_dequant_weights(const void* packed, int K, int N, int G, void* W,
                                      void* stream) {
+  return quick_dequant_weights_ex(packed, K, N, G, W, 0, stream);
+}
+
+quick_status_t quick_dequant_weights_ex(const void* packed, int K, int N, int G, void* W, int flags,
+                                        void* stream) {
+  if ((flags & ~QUICK_FLAG_BF16) != 0) return QUICK_ERR_UNSUPPORTED;
   quick_status_t st = check_gemm_shape(0, N, K, G);
   if (st != QUICK_OK) return st;
   if (!packed || !W) return QUICK_ERR_INVALID_ARG;
@@ -2049,8 +2141,12 @@ quick_status_t quick_dequant_weights(const void* packed, int K, int N, int G, vo
   const long long total = (long long)(N / 128) * (K / 32) * 128;
   const int threads = 256;
   const unsigned blocks = (unsigned)((total + threads - 1) / threads);
-  quick::quick_dequant_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const uint8_t*>(packed), static_cast<__half*>(W), K, N, G);
+  if (flags & QUICK_FLAG_BF16)
+    quick::quick_dequant_kernel<true><<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(packed), static_cast<uint16_t*>(W), K, N, G);
+  else
+    quick::quick_dequant_kernel<false><<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(packed), static_cast<uint16_t*>(W), K, N, G);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? QUICK_OK : cuda_fail(e);
 }

@@ -14,7 +14,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QUICK_LIB") or os.path.join(_PKG, "libquick.so")
 
 QUICK_OK, QUICK_ERR_INVALID_ARG, QUICK_ERR_UNSUPPORTED, QUICK_ERR_CUDA = 0, 1, 2, 3
-QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL, QUICK_FLAG_NO_STREAMK, QUICK_FLAG_SILU_MUL = 1, 2, 4, 8
+QUICK_FLAG_OUT_F32, QUICK_FLAG_PDL, QUICK_FLAG_NO_STREAMK, QUICK_FLAG_SILU_MUL, QUICK_FLAG_BF16 = 1, 2, 4, 8, 16
 
 
 class QuickError(RuntimeError):
@@ -48,6 +48,7 @@ def _load():
         "quick_gemm_plan": (c_int, [c_int, c_int, c_int, c_int, c_int, c_size_t, c_void_p, c_void_p, c_void_p,
                                     c_void_p]),
         "quick_dequant_weights": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
+        "quick_dequant_weights_ex": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p]),
         "quick_f32_to_f16": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
         "quick_gather_columns": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]),
         "quick_peer_alloc": (c_int, [c_size_t, c_void_p]),
@@ -259,14 +260,17 @@ def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ld
     workspace: optional zeroed cuda uint8 tensor (quick_workspace_bytes) enabling stream-K plans.
     Returns `out` (allocated if None): fp16 [M][N] (fp32 if out_fp32)."""
     import torch
-    if not (x.is_cuda and x.dtype == torch.float16 and x.is_contiguous() and x.dim() == 2 and x.shape[1] == K):
-        raise ValueError(f"x must be a contiguous cuda float16 [M][{K}] tensor")
+    if x.dtype == torch.bfloat16:          # the bf16 variant: bf16 X, scales (in the blob) and Y
+        flags |= QUICK_FLAG_BF16
+    if not (x.is_cuda and x.dtype in (torch.float16, torch.bfloat16) and x.is_contiguous() and x.dim() == 2
+            and x.shape[1] == K):
+        raise ValueError(f"x must be a contiguous cuda float16 / bfloat16 [M][{K}] tensor")
     if not (packed.is_cuda and packed.dtype == torch.uint8 and packed.is_contiguous()):
         raise ValueError("packed must be a contiguous cuda uint8 tensor")
     if packed.numel() != quick_packed_bytes(K, N, group_size):
         raise ValueError(f"packed has {packed.numel()} bytes, expected {quick_packed_bytes(K, N, group_size)}")
     M = x.shape[0]
-    want = torch.float32 if out_fp32 else torch.float16
+    want = torch.float32 if out_fp32 else x.dtype
     n_out = N // 2 if (flags & QUICK_FLAG_SILU_MUL) else N
     if out is None:
         out = torch.empty((M, n_out), device=x.device, dtype=want)
@@ -303,13 +307,13 @@ def quick_w4a16_gemm_raw(x_ptr: int, packed_ptr: int, M: int, N: int, K: int, gr
                                                      ctypes.c_void_p(stream_handle)))
 
 
-def quick_dequant_weights(packed, K: int, N: int, group_size: int, out=None, stream=None):
+def quick_dequant_weights(packed, K: int, N: int, group_size: int, out=None, stream=None, bf16: bool = False):
     import torch
     if out is None:
-        out = torch.empty((K, N), device=packed.device, dtype=torch.float16)
-    _check("quick_dequant_weights", _lib.quick_dequant_weights(ctypes.c_void_p(packed.data_ptr()), K, N, group_size,
-                                                               ctypes.c_void_p(out.data_ptr()),
-                                                               _stream_handle(stream)))
+        out = torch.empty((K, N), device=packed.device, dtype=torch.bfloat16 if bf16 else torch.float16)
+    _check("quick_dequant_weights_ex", _lib.quick_dequant_weights_ex(
+        ctypes.c_void_p(packed.data_ptr()), K, N, group_size, ctypes.c_void_p(out.data_ptr()),
+        QUICK_FLAG_BF16 if bf16 else 0, _stream_handle(stream)))
     return out
 
 

@@ -23,9 +23,11 @@ from .awq_inputs import (
     make_structured,
     GPTQProblem,
     make_gptq_problem,
+    make_problem_bf16,
 )
 
 __all__ = [
     "splitmix64", "uniform01", "AWQProblem", "make_x", "make_qweight", "make_zeros",
     "make_scales", "make_problem", "make_structured", "GPTQProblem", "make_gptq_problem",
+    "make_problem_bf16",
 ]

@@ -130,3 +130,19 @@ def make_gptq_problem(seed: int, M: int, N: int, K: int, G: int = 128, act_order
         order = np.argsort(splitmix64(_stream_seed(seed, 9), K), kind="stable")
         g_idx = g_idx[order].astype(np.int32)
     return GPTQProblem(x, qweight, qzeros, scales, g_idx, G)
+
+
+def _to_bf16_bits_trunc(v: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns of float32 values truncated toward zero (input construction only: no rounding
+    arithmetic of the method lives here)."""
+    return (np.asarray(v, dtype=np.float32).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def make_problem_bf16(seed: int, M: int, N: int, K: int, G: int = 128) -> AWQProblem:
+    """The bf16 variant's inputs: x and scales as bf16 BIT PATTERNS (uint16; numpy has no bf16):
+    X ~ U[-1, 1] and s ~ U[0.004, 0.012] truncated to bf16; codes and zeros as make_problem."""
+    u = uniform01(_stream_seed(seed, T_X), M * K)
+    x = _to_bf16_bits_trunc(2.0 * u - 1.0).reshape(M, K)
+    us = uniform01(_stream_seed(seed, T_SCALES), (K // G) * N)
+    s = _to_bf16_bits_trunc(0.004 + 0.008 * us).reshape(K // G, N)
+    return AWQProblem(x, make_qweight(seed, K, N), s, make_zeros(seed, K, N, G), G)

@@ -667,3 +667,54 @@ def test_gptq_import_gemm(M, K, N, G, act):
     w = oracle.gptq_dequant(p.qweight, p.qzeros, p.scales, g_idx=p.g_idx if act else None, group_size=G)
     res = oracle.tol_check(y.float().cpu().numpy(), oracle.gemm(p.x, w))
     assert res["ok"], res
+
+
+# ------------------------------------------------------------------------------- f3: the bf16 variant
+def _bf16_dev(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).to(DEV)
+
+
+def _bf16_ref(p):
+    w = oracle.dequant_bf16(p.qweight, p.scales, p.zeros, p.group_size)
+    return oracle.gemm_f64(oracle.bf16_from_bits(p.x), w)
+
+
+@pytest.mark.parametrize("K,N,G", [(512, 256, 128), (256, 384, 32), (192, 256, 96)])
+def test_bf16_dequant_bit_exact(K, N, G):
+    p = synth.make_problem_bf16(K ^ N, M=1, N=N, K=K, G=G)
+    blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).to(DEV)
+    w = quick.quick_dequant_weights(blob, K, N, G, bf16=True)
+    torch.cuda.synchronize()
+    ref = oracle.bf16_bits(oracle.dequant_bf16(p.qweight, p.scales, p.zeros, G))
+    np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16), ref)
+
+
+@pytest.mark.parametrize("M,tile_n,split_k", [(8, 0, 0), (1, 16, 4), (17, 32, 3), (64, 64, 2), (100, 128, 1),
+                                              (300, 256, 2), (200, 0, 0), (1024, 0, 0)])
+def test_bf16_gemm(M, tile_n, split_k):
+    """The bf16 variant (X, scales, Y bf16; oracle O9) across the plan families, incl. stream-K (workspace)
+    and CTA pairs (automatic plan at M = 200 / 1024)."""
+    N, K, G = (1024, 2048, 128) if M >= 200 else (512, 1024, 128)
+    p = synth.make_problem_bf16(M + 5, M=M, N=N, K=K, G=G)
+    blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).to(DEV)
+    y = quick.quick_w4a16_gemm(_bf16_dev(p.x), blob, N, K, G, tile_n=tile_n, split_k=split_k, workspace=WS)
+    torch.cuda.synchronize()
+    assert y.dtype == torch.bfloat16
+    res = oracle.tol_check(y.float().cpu().numpy(), _bf16_ref(p))
+    assert res["ok"], res
+
+
+def test_bf16_onehot_bit_exact_and_fp32_out():
+    """One-hot X picks rows of the bf16-dequantized weights exactly; the fp32 output of a random problem is
+    within fp32 accumulation error of the fp64 reference."""
+    p = synth.make_problem_bf16(3, M=16, N=256, K=512, G=128)
+    x = np.zeros((16, 512), dtype=np.uint16)
+    rows = np.arange(16) * 31 % 512
+    x[np.arange(16), rows] = 0x3F80                       # bf16 1.0
+    blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, 128)).to(DEV)
+    y = quick.quick_w4a16_gemm(_bf16_dev(x), blob, 256, 512, 128)
+    y32 = quick.quick_w4a16_gemm(_bf16_dev(p.x), blob, 256, 512, 128, out_fp32=True)
+    torch.cuda.synchronize()
+    w = oracle.dequant_bf16(p.qweight, p.scales, p.zeros, 128)
+    np.testing.assert_array_equal(y.cpu().view(torch.int16).numpy().view(np.uint16), oracle.bf16_bits(w[rows]))
+    assert np.max(np.abs(y32.cpu().numpy() - _bf16_ref(p))) < 1e-4

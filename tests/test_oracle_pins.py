@@ -401,3 +401,69 @@ def test_gptq_v2_without_act_order_is_the_awq_dequant():
     w_gptq = oracle.gptq_dequant(qweight, qzeros, p.scales, group_size=32, zero_plus_one=False)
     w_awq = oracle.dequant(p.qweight, p.scales, p.zeros, 32)
     assert np.array_equal(w_gptq.view(np.uint16), w_awq.view(np.uint16))
+
+
+# ------------------------------------------------------------------ O9 bf16 (R18)
+def _rne_bits_exact(fr: Fraction, p: int = 8):
+    """round-to-nearest-even of a positive Fraction to p significant bits, exactly (Fraction result)."""
+    e = 0
+    while fr >= 2:
+        fr /= 2
+        e += 1
+    while fr < 1:
+        fr *= 2
+        e -= 1
+    scaled = fr * (1 << (p - 1))
+    n = scaled.numerator // scaled.denominator
+    rem = scaled - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    return Fraction(n) / (1 << (p - 1)) * (Fraction(2) ** e)
+
+
+def test_bf16_rne_against_torch_and_exact_rounding():
+    """bf16_rne == torch's float32 -> bfloat16 conversion (library, round-to-nearest-even) on random fp32
+    values, ties included; and == exact rational RNE to 8 bits on hand-picked ties."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(5)
+    bits = rng.integers(0x3000_0000, 0x4F00_0000, 20000, dtype=np.uint32)
+    bits[:2000] = (bits[:2000] & np.uint32(0xFFFF0000)) | np.uint32(0x8000)   # exact ties
+    vals = bits.view(np.float32)
+    ref = torch.from_numpy(vals.copy()).to(torch.bfloat16).to(torch.float64).numpy()
+    got = oracle.bf16_rne(vals.astype(np.float64))
+    assert np.array_equal(got, ref)
+    for v in (Fraction(257, 256), Fraction(259, 256), Fraction(3, 1) + Fraction(1, 64), Fraction(12345, 1024)):
+        assert oracle.bf16_rne(float(v)) == float(_rne_bits_exact(v))
+
+
+def test_bf16_dequant_exhaustive_codes():
+    """Every (q, z) against 64 bf16 scales: bf16_rne((q - z) s) equals exact rational RNE, with the sign."""
+    K, N, G = 16, 64 * 16, 16
+    sbits = np.arange(64, dtype=np.uint16) * np.uint16(0x0103) + np.uint16(0x3A00)   # assorted positive scales
+    cols = np.arange(N)
+    z = (cols % 16).astype(np.uint8)
+    s = sbits[(cols // 16) % 64]
+    codes = np.tile((np.arange(K) % 16).astype(np.uint8)[:, None], (1, N))
+    w = oracle.dequant_bf16(oracle.pack_awq(codes), s[None, :], oracle.pack_awq(z[None, :]), G)
+    sv = oracle.bf16_from_bits(s)
+    for k in range(K):
+        for n in range(0, N, 7):
+            d = int(codes[k, n]) - int(z[n])
+            exact = Fraction(d) * Fraction(float(sv[n]))
+            want = 0.0 if d == 0 else float(_rne_bits_exact(abs(exact))) * (1 if d > 0 else -1)
+            assert w[k, n] == want, (k, n, d, sv[n])
+
+
+def test_bf16_gemm_integer_exact_regime():
+    """Small-integer X and power-of-two bf16 scales: every partial sum is exact, so O9's GEMM equals the
+    int64 matmul of codes scaled once."""
+    rng = np.random.default_rng(9)
+    K, N, M, G = 256, 128, 4, 128
+    codes = rng.integers(0, 16, (K, N))
+    zeros = rng.integers(0, 16, (K // G, N))
+    sb = np.full((K // G, N), 0x3C00, dtype=np.uint16)    # bf16 bits of 2^-7
+    x = rng.integers(-2, 3, (M, K)).astype(np.float64)
+    w = oracle.dequant_bf16(oracle.pack_awq(codes), sb, oracle.pack_awq(zeros), G)
+    y = oracle.gemm_f64(x, w)
+    ref = (x.astype(np.int64) @ (codes - zeros[np.arange(K) // G]).astype(np.int64)).astype(np.float64) * 2.0 ** -7
+    assert np.array_equal(y, ref)
