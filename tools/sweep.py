@@ -19,6 +19,8 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import _ws  # noqa: E402  (caller-owned stream-K workspace)
 
 SHAPES = {"small": [(4096, 4096)],
+          "mistral": [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)],
+          "fig7": [(8192, 8192)],
           "big": [(28672, 8192), (8192, 28672)],
           "all": [(4096, 4096), (13824, 5120), (5120, 13824), (28672, 8192), (8192, 28672)]}
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
