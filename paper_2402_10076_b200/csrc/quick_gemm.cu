@@ -848,12 +848,21 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         int as = iw % kAStages;
         uint32_t aph = (uint32_t)((iw / kAStages) & 1);
         const uint32_t sub_off = (uint32_t)(sub * 4 * kChunkBytes);
+        // shared-memory addresses of this warp's slot, advanced incrementally with the slot (no
+        // per-stage multiplies: the dequant is bound by the FMA pipe, where IMADs also issue)
+        uint32_t wslot = wrow + (uint32_t)(slot * C::W_BYTES) + sub_off;
+        uint32_t mslot = (uint32_t)(slot * C::M_BYTES);
+        uint32_t acol_as = tmem + tlane + (uint32_t)(as * kAColsPerStage);
+        // G == 128 (one group per A stage, the BJ value): the stage's group is block `sub` of its
+        // load stage's metadata, so the constants need no group arithmetic
+        const bool g128 = GBIG && gsh == 7;
+        const uint32_t msub = (uint32_t)sub * kMetaBytes;
         for (int a = sg.a_lo + rel0; a < sg.a_hi; a += NPAR, iw += NPAR) {
           const int ka = a * kKA;
           ptx::mbar_wait(bar_full + 8 * slot, fph);
           if (tw) stamp(2, iw);
-          const uint32_t wp = wrow + (uint32_t)(slot * C::W_BYTES) + sub_off;
-          const uint32_t moff = (uint32_t)(slot * C::M_BYTES);
+          const uint32_t wp = wslot;
+          const uint32_t moff = mslot;
           const int g0 = GBIG ? ((ka - sub * kKA) >> gsh) : group_of(ka - sub * kKA);
           // all four 16-B chunks: a short last stage (K % 128 == 64) reads two stale chunks of
           // its own slot and ignores them
@@ -864,10 +873,14 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           w[3] = ptx::lds128(wp + 3 * kChunkBytes);
           DequantConsts cst1;
           if constexpr (GBIG) {
-            const int g = ka >> gsh;
-            if (g != g_prev) {
-              cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
-              g_prev = g;
+            if (g128) {
+              cst = consts_at(moff + msub);
+            } else {
+              const int g = ka >> gsh;
+              if (g != g_prev) {
+                cst = consts_at(moff + (uint32_t)(g - g0) * kMetaBytes);
+                g_prev = g;
+              }
             }
           } else {
             cst = consts_at(moff + (uint32_t)(group_of(ka) - g0) * kMetaBytes);
@@ -893,7 +906,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             ptx::mbar_wait(bar_aempty + 8 * as, aph ^ 1u);
             if (tw) stamp(3, iw);
             ptx::tc_fence_after();
-            const uint32_t acol = tmem + tlane + (uint32_t)(as * kAColsPerStage);
+            const uint32_t acol = acol_as;
             if (dbg_nosttm) {   // keep the dequant live without storing it
               uint32_t x = 0;
 #pragma unroll
@@ -953,13 +966,19 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             if (tw) stamp(4, iw);
           }
           slot += NPAR / APL;
+          wslot += (uint32_t)((NPAR / APL) * C::W_BYTES);
+          mslot += (uint32_t)((NPAR / APL) * C::M_BYTES);
           if (slot >= STAGES) {
             slot -= STAGES;
+            wslot -= (uint32_t)(STAGES * C::W_BYTES);
+            mslot -= (uint32_t)(STAGES * C::M_BYTES);
             fph ^= 1u;
           }
           as += NPAR;
+          acol_as += (uint32_t)(NPAR * kAColsPerStage);
           if (as >= kAStages) {
             as -= kAStages;
+            acol_as -= (uint32_t)(kAStages * kAColsPerStage);
             aph ^= 1u;
           }
         }
