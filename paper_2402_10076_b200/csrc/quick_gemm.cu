@@ -524,7 +524,10 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     // The whole warp runs the (warp-uniform) loop; one elected lane issues the copies, so the
     // addresses stay in uniform registers and no per-lane waterfall is generated.  Load
     // stages never straddle segments (the last one of a segment may be short).
-    const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
+    // weights: streamed once per wave of m-tiles (evict-normal for m_tiles > 1 was measured 1-2 %
+    // slower on the 70B shapes at M >= 128 without fixing the M = 1024 DRAM re-reads,
+    // profiles/r02_l2_policy_ab.txt)
+    const uint64_t pol_w = ptx::policy_evict_first();
     const uint64_t pol_x = ptx::policy_evict_last();   // X: re-read by every n-tile
     SegIter it(p, SK, C::PAIR);
     Seg sg;
