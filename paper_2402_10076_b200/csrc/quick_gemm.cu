@@ -63,6 +63,12 @@ constexpr int kAblationSmemA = 1 << 21;    // ablation: A stage via shared memor
 constexpr int kForcePair = 1 << 20;        // debug: CTA-pair (cta_group::2) plan for tiles 128/256
 constexpr int kDebugNoPair = 1 << 19;      // debug: automatic plan without CTA pairs
 constexpr int kDebugForceSk = 1 << 17;     // debug: stream-K whenever the tile allows it
+constexpr int kDebugSkReverse = 1 << 16;   // debug: stream-K CTA c takes the unit range of CTA P-1-c
+
+// the stream-K "CTA index" that owns unit ranges (blockIdx.x, or reversed under kDebugSkReverse)
+__device__ __forceinline__ int sk_cta(int flags) {
+  return (flags & kDebugSkReverse) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x;
+}
 
 // Per tile width BN (tokens per MMA) and mode SK (stream-K):
 //   KL     k per load stage: one bulk copy of KL x 64 B of weights, one bulk copy of the groups'
@@ -176,10 +182,39 @@ struct KParams {
   // (32-bit, no division on the device); partial tiles go through ws and are summed by the
   // last arriver
   int U, P, sk_q, sk_r;
+  // placement-weighted stream-K (sk_wa > 0: CTAs [0, sk_h) take sk_wa / sk_wb times the units of the
+  // others).  Measured on B200 with the first-placed CTA of each SM weighted 1.05-1.2x: slower at every
+  // weight (profiles/r02_sk_placement.txt), so the host always launches uniform ranges (sk_wa = 0)
+  int sk_wa, sk_wb, sk_h;
   float* ws;              // [P][BN][128] fp32 partial tile of each CTA's (only) non-reducer segment
   int* sems;              // [tiles] arrival counters, zero between launches (reset by the reducer)
   unsigned long long* trace;
 };
+
+__device__ __forceinline__ int sk_start(int c, int q, int r) { return c * q + min(c, r); }
+// first unit of stream-K CTA c (c = P: U), uniform or placement-weighted (KParams::sk_wa)
+__device__ __forceinline__ int sk_begin(const KParams& p, int c) {
+  if (p.sk_wa == 0) return sk_start(c, p.sk_q, p.sk_r);
+  const long long wsum = (long long)p.sk_wa * p.sk_h + (long long)p.sk_wb * (p.P - p.sk_h);
+  const long long cum = c <= p.sk_h ? (long long)p.sk_wa * c
+                                    : (long long)p.sk_wa * p.sk_h + (long long)p.sk_wb * (c - p.sk_h);
+  return (int)(((long long)p.U * cum) / wsum);
+}
+// the stream-K CTA owning unit u (the largest c with sk_begin(c) <= u)
+__device__ __forceinline__ int sk_owner(const KParams& p, int u) {
+  if (p.sk_wa == 0) {
+    const int b = p.sk_r * (p.sk_q + 1);
+    return u < b ? u / (p.sk_q + 1) : p.sk_r + (u - b) / p.sk_q;
+  }
+  const long long wsum = (long long)p.sk_wa * p.sk_h + (long long)p.sk_wb * (p.P - p.sk_h);
+  const long long t = ((long long)u * wsum) / p.U;   // ~ cum(c) at unit u
+  const long long ta = (long long)p.sk_wa * p.sk_h;
+  int c = t < ta ? (int)(t / p.sk_wa) : p.sk_h + (int)((t - ta) / p.sk_wb);
+  if (c > p.P - 1) c = p.P - 1;
+  while (c > 0 && sk_begin(p, c) > u) --c;
+  while (c + 1 < p.P && sk_begin(p, c + 1) <= u) ++c;
+  return c;
+}
 
 // One contiguous run of A stages [a_lo, a_hi) of one tile (n-tile t, m-tile mt).
 struct Seg {
@@ -202,9 +237,9 @@ struct SegIter {
     m_tiles = p.m_tiles;
     done = false;
     if (sk) {
-      const int c = (int)blockIdx.x;
-      u = c * p.sk_q + min(c, p.sk_r);
-      u1 = u + p.sk_q + (c < p.sk_r ? 1 : 0);
+      const int c = sk_cta(p.flags);
+      u = sk_begin(p, c);
+      u1 = sk_begin(p, c + 1);
     } else {
       const int S = pair ? (int)gridDim.x >> 1 : (int)gridDim.x;
       const int sp = pair ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
@@ -242,12 +277,6 @@ struct SegIter {
   }
 };
 
-// stream-K bookkeeping (U = P q + r, KParams): a CTA's first unit, and the CTA owning unit u
-__device__ __forceinline__ int sk_start(int c, int q, int r) { return c * q + min(c, r); }
-__device__ __forceinline__ int sk_cta_of(int u, int q, int r) {
-  const int b = r * (q + 1);   // units owned by the r CTAs with q + 1 units
-  return u < b ? u / (q + 1) : r + (u - b) / q;
-}
 
 // ------------------------------------------------------------------------------------------
 // Dequantization of one 32-bit word of the v1 layout (8 codes, nibble order {0,2,4,6,1,3,5,7}
@@ -361,7 +390,8 @@ __device__ __forceinline__ uint32_t cvt16x2(float a, float b) {
 
 // SiLU(g) * u in fp32 (the fused gate||up epilogue, QUICK_FLAG_SILU_MUL)
 __device__ __forceinline__ float silu_mul(float g, float u) {
-  return g * __frcp_rn(1.0f + __expf(-g)) * u;
+  // MUFU exp2 + fast reciprocal-division (~2 ulp in fp32; the result is rounded to 16 bits)
+  return __fdividef(g * u, 1.0f + __expf(-g));
 }
 
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B (SBO), version 1
@@ -1037,13 +1067,17 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 #pragma unroll 1
        for (int d = 0; d < p.ndst; ++d) {
         void* Yb = p.Ydst[d];
-        if (silu) {   // warp-uniform: every lane shuffles, the gate lanes store
-          uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
+        if (silu) {   // warp-uniform: every lane shuffles; gate lanes store even tokens, up lanes odd
+          float x[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float u = __shfl_xor_sync(0xffffffffu, f[i], 16);
-            if (i < cnt && silu_store) *yp = cvt16<BF>(silu_mul(f[i], u));
-            yp += p.ldy;
+          for (int i = 0; i < 8; ++i) x[i] = __shfl_xor_sync(0xffffffffu, f[i], 16);
+          uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc + (silu_store ? 0 : 1)) * p.ldy + n;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float g = silu_store ? f[2 * j] : x[2 * j + 1];
+            const float u = silu_store ? x[2 * j] : f[2 * j + 1];
+            if (2 * j + (silu_store ? 0 : 1) < cnt) *yp = cvt16<BF>(silu_mul(g, u));
+            yp += 2 * p.ldy;
             asm volatile("" : "+l"(yp));
           }
         } else if (out_fp32) {
@@ -1082,13 +1116,18 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
          for (int d = 0; d < p.ndst; ++d) {
           void* Yb = p.Ydst[d];
           if (silu) {
-            uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
+            // the partner lane's values, then gate lanes take the even tokens and up lanes the odd
+            // ones (each lane computes and stores half of the 32 SiLU*mul results)
+            uint32_t x[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float g = __uint_as_float(v[i]);
-              const float u = __shfl_xor_sync(0xffffffffu, g, 16);
-              if (i < cnt && silu_store) *yp = cvt16<BF>(silu_mul(g, u));
-              yp += p.ldy;
+            for (int i = 0; i < 32; ++i) x[i] = __shfl_xor_sync(0xffffffffu, v[i], 16);
+            uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc + (silu_store ? 0 : 1)) * p.ldy + n;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float g = __uint_as_float(silu_store ? v[2 * j] : x[2 * j + 1]);
+              const float u = __uint_as_float(silu_store ? x[2 * j] : v[2 * j + 1]);
+              if (2 * j + (silu_store ? 0 : 1) < cnt) *yp = cvt16<BF>(silu_mul(g, u));
+              yp += 2 * p.ldy;
               asm volatile("" : "+l"(yp));
             }
           } else if (out_fp32) {
@@ -1150,11 +1189,11 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         // waiting; c_first waits (rarely for long) for all of them, adds their partials in CTA
         // order to its own accumulator (straight from TMEM) and writes Y.  Deterministic.
         const int u_first = sg.tile * p.NA;
-        const int c_first = sk_cta_of(u_first, p.sk_q, p.sk_r);
-        const int c_last = sk_cta_of(u_first + p.NA - 1, p.sk_q, p.sk_r);
+        const int c_first = sk_owner(p, u_first);
+        const int c_last = sk_owner(p, u_first + p.NA - 1);
         int* sem = p.sems + sg.tile;
-        if ((int)blockIdx.x != c_first) {
-          float* slot_ws = p.ws + (size_t)blockIdx.x * (BN * kTileRows);
+        if (sk_cta(p.flags) != c_first) {
+          float* slot_ws = p.ws + (size_t)sk_cta(p.flags) * (BN * kTileRows);
 #pragma unroll 1
           for (int jc = j0; jc < jmax; jc += 8) {
             uint32_t v[8];
@@ -1919,7 +1958,8 @@ constexpr int kKnownFlags = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_
                             quick::kDebugNoCompute |
                             quick::kDebugExitTop | quick::kDebugExitPrologue | quick::kDebugNoMma |
                             quick::kDebugOneCta | quick::kDebugNoSttm | quick::kDebugPdlEarly |
-                            quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair | quick::kDebugForceSk;
+                            quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair | quick::kDebugForceSk |
+                            quick::kDebugSkReverse;
 
 // The launch plan of a call: a pure function of the shape, flags and overrides, and of whether
 // a stream-K workspace may be used (`allow_ws`).
