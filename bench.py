@@ -177,7 +177,8 @@ def run_quick(args, rank, world, dist):
     import torch
     from paper_2402_10076_b200 import quick, tp
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    # (--dist-backend gloo, a test mode: several ranks may share one GPU)
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     cfg_idx, shapes, Ms, G = WORKLOADS[args.workload]
     props = torch.cuda.get_device_properties(dev)
@@ -322,7 +323,7 @@ def run_quick(args, rank, world, dist):
         return graphs
 
     K_steps, W = args.steps, args.warmup
-    coll_in_graph = world > 1
+    coll_in_graph = world > 1 and (peer or args.dist_backend == "nccl")   # gloo collectives cannot be captured
     try:
         graphs_full = build_graphs(BLOCK_C, coll_in_graph)
     except Exception:        # a NCCL build that cannot be captured: collectives run eagerly
@@ -714,6 +715,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="N > 1 process group: nccl (the measurement); gloo only to exercise the N > 1 code paths "
+                         "with several ranks on one GPU (CUDA tensors through gloo, collectives not captured)")
     ap.add_argument("--comm", choices=["nccl", "peer"], default="nccl",
                     help="N > 1: NCCL collectives after the GEMMs, or the collective-fused peer-memory TP GEMMs")
     args = ap.parse_args()
@@ -740,8 +744,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        tdist.init_process_group(args.dist_backend)
         if tdist.get_world_size() != args.gpus:
             sys.exit("bench.py: process group size != --gpus")
         dist = tdist
