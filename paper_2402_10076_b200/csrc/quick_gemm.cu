@@ -100,7 +100,7 @@ struct Cfg {
   static constexpr int THREADS = 32 * (4 * NPAR + 2);
   // warp roles: dequant warps 0..4 NPAR - 1, then the producer and the MMA warp.  The build
   // variant QUICK_ROLES_FIRST puts the producer / MMA warps at ids 0 / 1 instead: measured equal
-  // on B200 over the BJ shapes x M = 1..1024 (tools/gpu_r2_t6.sh, profiles/r02_warp_roles_ab.txt),
+  // on B200 over the BJ shapes x M = 1..1024 (tools/gpu_r2_experiments.sh warp_roles, profiles/r02_warp_roles_ab.txt),
   // and equally imbalanced between the two co-resident stream-K CTAs
 #ifdef QUICK_ROLES_FIRST
   static constexpr int DQ_BASE = 2;
