@@ -120,12 +120,16 @@ struct Cfg {
                 : (BN == 256 ? 4 : BN > 64 ? 2 : ((256 - NDBUF * BN) / kAColsPerStage >= 3 ? 3 : 2));
   static constexpr int DCOL = !SMEM_A ? ASTAGES * kAColsPerStage : 0;   // A ring columns in TMEM
   static constexpr int NACC = (BN <= 32 && DCOL + NDBUF * 2 * BN <= TMEM_BUDGET) ? 2 : 1;
-  static constexpr int KL = BN <= 32 ? 256 : 128;
+  // (the 16-token stream-K tile streams 8 KiB load stages through an 8-deep ring: each slot is
+  // released after one A stage instead of two, so more of the ring is in flight -- 28672x8192 and
+  // 8192x28672 at M <= 16: 31.1 -> 29.5 us; the cluster split-K tile-16 plans, with few stages
+  // per CTA, keep 256-k stages: 4096^2 M = 1 6.4 vs 7.1 us with 128)
+  static constexpr int KL = (BN <= 16 && SK) ? 128 : BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
   static constexpr int STAGES = NPAR == 4 ? (BN <= 16 ? 8 : BN <= 32 ? 6 : 8)
-                                          : (BN <= 16 ? 4 : BN <= 32 ? 3 : BN <= 128 ? (SMEM_A ? 3 : 4)
+                                          : (BN <= 16 ? (KL == 128 ? 8 : 4) : BN <= 32 ? 3 : BN <= 128 ? (SMEM_A ? 3 : 4)
                                                                                    : (PAIR ? 4 : 3));
   static constexpr int X_BYTES = XN * KL * 2;       // [KL/64][XN][64] fp16, SW128 sub-tiles
   static constexpr int X_SUB = XN * 128;            // one [XN][64] sub-tile (multiple of 1 KiB)
@@ -890,7 +894,103 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
         // load stage's metadata, so the constants need no group arithmetic
         const bool g128 = GBIG && gsh == 7;
         const uint32_t msub = (uint32_t)sub * kMetaBytes;
-        for (int a = sg.a_lo + rel0; a < sg.a_hi; a += NPAR, iw += NPAR) {
+        // Lean steady-state loop (G a power of two >= 128, A in TMEM): the instruction count per
+        // A stage is what bounds the small-M decode (ncu: ~300 warp instructions per warp-stage,
+        // 208 of them the dequantization).  Here: one barrier register per ring (full/empty and
+        // afull/aempty are constant offsets apart), waits as single asm loops, the stage's metadata
+        // block folded into one running address, the arrival count and short-stage tests
+        // precomputed per segment.
+        // (G == 128 only: a larger power-of-two group can straddle a load stage's two A stages, which
+        // the general loop below handles)
+        bool lean = false;
+        if constexpr (GBIG && AM == 0) lean = !dbg_nosttm && !dbg_nocompute && g128;
+        if (lean) {
+          const int a_end = sg.a_hi;
+          // K % 128 == 64: the segment's last A stage holds one half (64 k) only
+          const int a_short = (k_seg_end & (kKA - 1)) != 0 ? a_end - 1 : 0x7fffffff;
+          // a load stage holding a single A stage (segment end): this thread also arrives for the
+          // other parity's share
+          const int a_cnt2 = (APL == 2 && sub == 0) ? a_end - 1 : 0x7fffffff;
+          // ring positions are kept as (slot, phase) pairs only; the barrier, shared-memory and
+          // TMEM addresses are re-derived from them each stage (LEA / one IMAD: fewer live
+          // registers and no loop-carried address copies)
+          const uint32_t wbase = wrow + sub_off;                    // + slot x W_BYTES
+          const uint32_t mbase = mrow + msub;                       // + slot x M_BYTES
+          const uint32_t zdelta = zrow - mrow;
+          const uint32_t abase = tmem + tlane;                      // + as x 64 columns
+          for (int a = sg.a_lo + rel0; a < a_end; a += NPAR, iw += NPAR) {
+            const uint32_t fbar = bar_full + 8u * (uint32_t)slot;   // empty = fbar + 8 STAGES
+            const uint32_t wp = wbase + (uint32_t)slot * (uint32_t)C::W_BYTES;
+            const uint32_t maddr = mbase + (uint32_t)slot * (uint32_t)C::M_BYTES;
+            ptx::mbar_wait_loop(fbar, fph);
+            if (tw) stamp(2, iw);
+            uint4 w[4];
+            w[0] = ptx::lds128(wp);
+            w[1] = ptx::lds128(wp + kChunkBytes);
+            w[2] = ptx::lds128(wp + 2 * kChunkBytes);
+            w[3] = ptx::lds128(wp + 3 * kChunkBytes);
+            DequantConsts c;
+            {
+              const uint32_t zb = ptx::lds_u8(maddr + zdelta);
+              const uint32_t sbits = ptx::lds_u16(maddr);
+              const uint32_t zr = __byte_perm(zb, 0u, 0x4040);   // [zb, 0, zb, 0]
+              if constexpr (BF) {
+                c.zlo = ptx::lop3<0xEA>(zr >> zsh, 0x000F000Fu, 0x43004300u);
+                c.zhi = 0u;
+              } else {
+                c.zlo = ptx::lop3<0xEA>(zr >> zsh, 0x000F000Fu, 0x64006400u);
+                c.zhi = ptx::lop3<0xEA>(zr << zsh_hi, 0x00F000F0u, 0xD400D400u);
+              }
+              c.s2 = __byte_perm(sbits, 0u, 0x1010);
+            }
+            ptx::mbar_arrive_cnt(fbar + 8u * STAGES, a == a_cnt2 ? 2u : 1u);
+            dequant_w<BF>(w[0].x, c, a_regs + 0);
+            dequant_w<BF>(w[0].y, c, a_regs + 4);
+            dequant_w<BF>(w[0].z, c, a_regs + 8);
+            dequant_w<BF>(w[0].w, c, a_regs + 12);
+            dequant_w<BF>(w[1].x, c, a_regs + 16);
+            dequant_w<BF>(w[1].y, c, a_regs + 20);
+            dequant_w<BF>(w[1].z, c, a_regs + 24);
+            dequant_w<BF>(w[1].w, c, a_regs + 28);
+            const uint32_t abar = bar_afull + 8u * (uint32_t)as;   // aempty = abar + 8 kAStages
+            const uint32_t acol = abase + (uint32_t)as * (uint32_t)kAColsPerStage;
+            ptx::mbar_wait_loop(abar + 8u * kAStages, aph ^ 1u);
+            if (tw) stamp(3, iw);
+            ptx::tc_fence_after();
+            ptx::tmem_st_32x32b_x32(acol, a_regs);
+            if (a != a_short) {
+              uint32_t b_regs[32];
+              dequant_w<BF>(w[2].x, c, b_regs + 0);
+              dequant_w<BF>(w[2].y, c, b_regs + 4);
+              dequant_w<BF>(w[2].z, c, b_regs + 8);
+              dequant_w<BF>(w[2].w, c, b_regs + 12);
+              dequant_w<BF>(w[3].x, c, b_regs + 16);
+              dequant_w<BF>(w[3].y, c, b_regs + 20);
+              dequant_w<BF>(w[3].z, c, b_regs + 24);
+              dequant_w<BF>(w[3].w, c, b_regs + 28);
+              ptx::tmem_st_32x32b_x32(acol + 32, b_regs);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            if constexpr (kWarpArrive)
+              arrive_afull(as);
+            else
+              ptx::mbar_arrive(abar);
+            if (tw) stamp(4, iw);
+            // advance: the load ring by NPAR / APL slots, the A ring by NPAR slots
+            slot += NPAR / APL;
+            if (slot >= STAGES) {
+              slot -= STAGES;
+              fph ^= 1u;
+            }
+            as += NPAR;
+            if (as >= kAStages) {
+              as -= kAStages;
+              aph ^= 1u;
+            }
+          }
+        }
+        for (int a = sg.a_lo + rel0; !lean && a < sg.a_hi; a += NPAR, iw += NPAR) {
           const int ka = a * kKA;
           ptx::mbar_wait(bar_full + 8 * slot, fph);
           if (tw) stamp(2, iw);

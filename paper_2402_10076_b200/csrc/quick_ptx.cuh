@@ -73,6 +73,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// the same wait as one asm loop: TRYWAIT + a predicated branch to an out-of-line retry (a C++ loop
+// around try_wait makes the compiler wrap it in BSSY/BSYNC convergence barriers: 2-3 extra
+// instructions per wait in the dequant loop)
+__device__ __forceinline__ void mbar_wait_loop(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "QUICK_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni QUICK_WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 // try_wait with a suspend-time hint: the waiting warp is descheduled (up to the hint, in ns)
 // instead of spinning, so it takes no issue slots from the warps it shares an SMSP with
 __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {

@@ -78,11 +78,13 @@ for (N, K) in SHAPES[which]:
         for mode in modes:
             # "auto" / "pdl" / "nosk", or a forced plan "t<tile>s<split>[p]" (e.g. t256s2, t256s2p)
             fl, tn, sk = FLAGS.get(mode, 0), 0, 0
-            if mode.startswith("t"):   # "t<tile>s<split>[p]": p = CTA pair (cta_group::2)
+            if mode.startswith("t"):   # "t<tile>s<split>[p][e]": p = CTA pair (cta_group::2), e = early PDL trigger
                 fl = quick.QUICK_FLAG_PDL   # forced plans are timed with PDL, like the bench
-                if mode.endswith("p"):
+                if mode.endswith("e"):
+                    fl |= 1 << 24
+                if mode.rstrip("e").endswith("p"):
                     fl |= 1 << 20
-                tn, sk = (int(v) for v in mode[1:].rstrip("p").split("s"))
+                tn, sk = (int(v) for v in mode[1:].rstrip("e").rstrip("p").split("s"))
                 if tn > 2 * M and tn > 16:
                     continue
             us = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
