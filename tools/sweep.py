@@ -80,11 +80,14 @@ for (N, K) in SHAPES[which]:
             fl, tn, sk = FLAGS.get(mode, 0), 0, 0
             if mode.startswith("t"):   # "t<tile>s<split>[p][e]": p = CTA pair (cta_group::2), e = early PDL trigger
                 fl = quick.QUICK_FLAG_PDL   # forced plans are timed with PDL, like the bench
-                if mode.endswith("e"):
+                if mode.endswith("k"):   # k = force the stream-K schedule (split must be 0)
+                    fl |= 1 << 17
+                mm = mode.rstrip("k")
+                if mm.endswith("e"):
                     fl |= 1 << 24
-                if mode.rstrip("e").endswith("p"):
+                if mm.rstrip("e").endswith("p"):
                     fl |= 1 << 20
-                tn, sk = (int(v) for v in mode[1:].rstrip("e").rstrip("p").split("s"))
+                tn, sk = (int(v) for v in mm[1:].rstrip("e").rstrip("p").split("s"))
                 if tn > 2 * M and tn > 16:
                     continue
             us = timeit(lambda i: _ws.gemm_raw(x.data_ptr(), copies[i % R].data_ptr(), M, N, K, G,
