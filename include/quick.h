@@ -151,6 +151,20 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
                                    int split_k, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* quick_w4a16_gemm_ex with a bias epilogue (SURVEY 8(f) f2 "bias"; not in PAPER.md, whose
+ * mixed-precision GEMM of §2.3 P:L58-64 has none):
+ *   Y[m][n] = round16( sum_k X[m][k] . dequant(W)[k][n]  +  bias[n] )
+ * bias: device pointer to N 16-bit values (fp16; bf16 with QUICK_FLAG_BF16), 8-byte aligned,
+ * read-only, owned by the caller.  The bias is added in fp32 to the fp32 sum once, by the CTA
+ * that writes Y (after the split-K / stream-K reduction), then the result is rounded once to 16
+ * bits (or stored as fp32 with QUICK_FLAG_OUT_F32, bias included).  NULL bias -> INVALID_ARG;
+ * with QUICK_FLAG_SILU_MUL -> UNSUPPORTED (the gate||up blob has no bias layout).  Every other
+ * argument, rule and error as in quick_w4a16_gemm_ex. */
+quick_status_t quick_w4a16_gemm_bias(const void* X, const void* packed, const void* bias, int M, int N,
+                                     int K, int group_size, void* Y, int ldy, int flags, int tile_n,
+                                     int split_k, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
 /* The launch plan quick_w4a16_gemm_ex(M, N, K, G, flags, tile_n = 0, split_k = 0, workspace of
  * workspace_bytes) would use: tokens per tile, cluster split-K factor (0 = stream-K schedule),
  * number of CTAs, and 1 if the tiles run as CTA pairs.  Any out pointer may be NULL. */

@@ -19,6 +19,7 @@ from .quick_oracle import (  # noqa: F401
     w4a16_reference,
     round_fp16,
     silu_mul,
+    add_bias,
     gptq_dequant,
     bf16_rne,
     bf16_bits,

@@ -35,6 +35,9 @@ What the path computes (PAPER.md = /root/reference/PAPER.md, "P:L<n>" = its line
               not on its hot path -- DESIGN.md reading R16): h = SiLU(g) * u with
               SiLU(g) = g / (1 + exp(-g)) (the Llama/Mistral MLP activation), in fp64 on the
               two O3 results.
+  O10 bias    (SURVEY §8(f) f2 "bias"; not in PAPER.md -- DESIGN.md reading R21):
+              Y[m][n] = sum_k x[m][k] w[k][n] + b[n], the bias a 16-bit value added once to the
+              exact (fp64) O3 sum, then one rounding (O4).
 
 No blocking, fusion or reordering beyond the definitions above; numpy's fp64 matmul is the
 one library primitive used (as a step: a dot product in fp64).
@@ -161,6 +164,12 @@ def silu_mul(g: np.ndarray, u: np.ndarray) -> np.ndarray:
     u = np.asarray(u, dtype=np.float64)
     with np.errstate(over="ignore"):
         return g / (1.0 + np.exp(-g)) * u
+
+
+# ----------------------------------------------------------------------------------------- O10
+def add_bias(y: np.ndarray, bias) -> np.ndarray:
+    """O10: Y + b broadcast over the rows (fp64; b given as float16 / float64 values)."""
+    return np.asarray(y, dtype=np.float64) + np.asarray(bias, dtype=np.float64)[None, :]
 
 
 # ----------------------------------------------------------------------------------------- O4

@@ -96,7 +96,11 @@ struct Cfg {
   // for a 6-7 slot A ring) was measured 1.9x slower per SM than two 2-group CTAs per SM on the
   // 70B shapes at M <= 64 (one MMA warp per SM cannot keep up), so every tile uses 2 groups; the
   // code is written for any power-of-two NPAR.
+#ifdef QUICK_NPAR4
+  static constexpr int NPAR = (SK && BN <= 16) ? 4 : 2;   // probe variant: one 16-warp CTA per SM
+#else
   static constexpr int NPAR = 2;
+#endif
   static constexpr int THREADS = 32 * (4 * NPAR + 2);
   // warp roles: dequant warps 0..4 NPAR - 1, then the producer and the MMA warp.  The build
   // variant QUICK_ROLES_FIRST puts the producer / MMA warps at ids 0 / 1 instead: measured equal
@@ -124,7 +128,7 @@ struct Cfg {
   // released after one A stage instead of two, so more of the ring is in flight -- 28672x8192 and
   // 8192x28672 at M <= 16: 31.1 -> 29.5 us; the cluster split-K tile-16 plans, with few stages
   // per CTA, keep 256-k stages: 4096^2 M = 1 6.4 vs 7.1 us with 128)
-  static constexpr int KL = (BN <= 16 && SK) ? 128 : BN <= 32 ? 256 : 128;
+  static constexpr int KL = (BN <= 16 && SK && NPAR == 2) ? 128 : BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
@@ -193,6 +197,9 @@ struct KParams {
   float* ws;              // [P][BN][128] fp32 partial tile of each CTA's (only) non-reducer segment
   int* sems;              // [tiles] arrival counters, zero between launches (reset by the reducer)
   unsigned long long* trace;
+  // optional bias: [N] fp16 (bf16 with QUICK_FLAG_BF16) added in fp32 to every token's
+  // output column before the final rounding, by whichever CTA writes Y; nullptr = none
+  const uint16_t* bias;
 };
 
 __device__ __forceinline__ int sk_start(int c, int q, int r) { return c * q + min(c, r); }
@@ -390,6 +397,15 @@ __device__ __forceinline__ uint32_t cvt16x2(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+}
+
+// a 16-bit bias value (fp16, or bf16 for the bf16 variant) as fp32 (exact)
+template <bool BF>
+__device__ __forceinline__ float bias_f(uint16_t b) {
+  if constexpr (BF)
+    return __uint_as_float((uint32_t)b << 16);
+  else
+    return __half2float(__ushort_as_half(b));
 }
 
 // SiLU(g) * u in fp32 (the fused gate||up epilogue, QUICK_FLAG_SILU_MUL)
@@ -1125,6 +1141,8 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       const int m0 = sg.mt * BN;
       const int n = silu ? sg.t * (kTileRows / 2) + q * 16 + (lane & 15) : sg.t * kTileRows + r;
       const bool silu_store = (lane & 16) == 0;
+      // this thread's output column n gets bias[n] (plain outputs only: the host rejects bias + SiLU)
+      const float bv = p.bias != nullptr ? bias_f<BF>(p.bias[n]) : 0.0f;
       ptx::mbar_wait(bar_dfull + 8 * db, (uint32_t)((si >> 1) & 1));
       ptx::tc_fence_after();
       if (TRACE && tr != nullptr && warp == C::DQ_BASE && lane == 0) tr[1] = clock64();
@@ -1184,7 +1202,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           float* yp = reinterpret_cast<float*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (i < cnt) *yp = f[i];
+            if (i < cnt) *yp = f[i] + bv;
             yp += p.ldy;
             asm volatile("" : "+l"(yp));
           }
@@ -1192,7 +1210,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
           uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (i < cnt) *yp = cvt16<BF>(f[i]);
+            if (i < cnt) *yp = cvt16<BF>(f[i] + bv);
             yp += p.ldy;
             asm volatile("" : "+l"(yp));
           }
@@ -1234,7 +1252,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             float* yp = reinterpret_cast<float*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              if (i < cnt) *yp = __uint_as_float(v[i]);
+              if (i < cnt) *yp = __uint_as_float(v[i]) + bv;
               yp += p.ldy;
               asm volatile("" : "+l"(yp));
             }
@@ -1242,7 +1260,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             uint16_t* yp = reinterpret_cast<uint16_t*>(Yb) + (size_t)(m0 + jc) * p.ldy + n;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-              if (i < cnt) *yp = cvt16<BF>(__uint_as_float(v[i]));
+              if (i < cnt) *yp = cvt16<BF>(__uint_as_float(v[i]) + bv);
               yp += p.ldy;
               asm volatile("" : "+l"(yp));
             }
@@ -1373,10 +1391,18 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
       }
       return ptx::ld_dsmem_f32x4(peer[q] + (uint32_t)e * 4u);
     };
-    auto store_sum = [&](int e, const float4& acc) {
+    auto store_sum = [&](int e, const float4& acc_in) {
       const int j = e / kTileRows;
       const int rr = e % kTileRows;
       const size_t o = (size_t)(m0 + j) * p.ldy + (size_t)tt * kTileRows + rr;
+      float4 acc = acc_in;
+      if (p.bias != nullptr) {   // output columns tt x 128 + rr .. rr + 3
+        const uint2 b4 = *reinterpret_cast<const uint2*>(p.bias + (size_t)tt * kTileRows + rr);
+        acc.x += bias_f<BF>((uint16_t)(b4.x & 0xFFFFu));
+        acc.y += bias_f<BF>((uint16_t)(b4.x >> 16));
+        acc.z += bias_f<BF>((uint16_t)(b4.y & 0xFFFFu));
+        acc.w += bias_f<BF>((uint16_t)(b4.y >> 16));
+      }
       if (out_fp32) {
 #pragma unroll 1
         for (int d = 0; d < p.ndst; ++d)
@@ -2179,7 +2205,7 @@ namespace quick {
 // rank's column slot of that rank's Y).
 quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int K, int G, void* Y, int ldy,
                            int flags, int tile_n, int split_k, void* workspace, size_t workspace_bytes,
-                           void* const* ydst, int ndst, void* stream) {
+                           void* const* ydst, int ndst, void* stream, const void* bias) {
   quick_status_t st = check_gemm_shape(M, N, K, G);
   if (st != QUICK_OK) return st;
   if (M == 0) return QUICK_OK;
@@ -2189,6 +2215,7 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   if (ldy < (silu ? N / 2 : N)) return QUICK_ERR_INVALID_ARG;
   if (ldy % 8 != 0 || (flags & ~kKnownFlags) != 0) return QUICK_ERR_UNSUPPORTED;
   if (silu && (flags & (QUICK_FLAG_OUT_F32 | quick::kAblationSmemA))) return QUICK_ERR_UNSUPPORTED;
+  if (bias != nullptr && (silu || !aligned(bias, 8))) return QUICK_ERR_UNSUPPORTED;
   if ((flags & QUICK_FLAG_BF16) && (flags & quick::kAblationSmemA)) return QUICK_ERR_UNSUPPORTED;
   if (!aligned(X, 16) || !aligned(Y, 16) || !aligned(packed, 128)) return QUICK_ERR_UNSUPPORTED;
   if (workspace_bytes != 0 && (workspace == nullptr || !aligned(workspace, 256))) return QUICK_ERR_INVALID_ARG;
@@ -2224,6 +2251,7 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
 
   kp.packed = static_cast<const uint8_t*>(packed);
   kp.Y = Y;
+  kp.bias = static_cast<const uint16_t*>(bias);
   if (ndst < 1 || ndst > kMaxPeers) return QUICK_ERR_INVALID_ARG;
   kp.ndst = ndst;
   for (int d = 0; d < ndst; ++d) {
@@ -2242,7 +2270,11 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   kp.ldy = ldy;
   // the 256-token tile launches without programmatic dependent launch (an
   // intermittent fault with deeper PDL prefetch whose root cause is not established)
+#ifdef QUICK_PDL256
+  kp.flags = flags;   // build variant for probing the tile-256 PDL fault (tools/gpu_t256.sh)
+#else
   kp.flags = (tn == 256) ? (flags & ~QUICK_FLAG_PDL) : flags;
+#endif
   // A stream-K grid holding every CTA slot of the machine triggers its dependents right after the
   // prologue: the next GEMM's CTAs can only land in slots our CTAs vacate, so an early trigger
   // lets each one start (prologue, weight prefetch, first dequantized stages) as soon as a slot
@@ -2280,7 +2312,16 @@ quick_status_t quick_w4a16_gemm_ex(const void* X, const void* packed, int M, int
                                    void* workspace, size_t workspace_bytes, void* stream) {
   void* const dst[1] = {Y};
   return quick::gemm_launch(X, packed, M, N, K, G, Y, ldy, flags, tile_n, split_k, workspace, workspace_bytes,
-                            dst, 1, stream);
+                            dst, 1, stream, nullptr);
+}
+
+quick_status_t quick_w4a16_gemm_bias(const void* X, const void* packed, const void* bias, int M, int N, int K,
+                                     int G, void* Y, int ldy, int flags, int tile_n, int split_k,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (bias == nullptr) return QUICK_ERR_INVALID_ARG;
+  void* const dst[1] = {Y};
+  return quick::gemm_launch(X, packed, M, N, K, G, Y, ldy, flags, tile_n, split_k, workspace, workspace_bytes,
+                            dst, 1, stream, bias);
 }
 
 quick_status_t quick_w4a16_gemm(const void* X, const void* packed, int M, int N, int K, int G,

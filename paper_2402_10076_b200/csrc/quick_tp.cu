@@ -30,7 +30,7 @@
 namespace quick {
 quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int K, int G, void* Y, int ldy,
                            int flags, int tile_n, int split_k, void* workspace, size_t workspace_bytes,
-                           void* const* ydst, int ndst, void* stream);
+                           void* const* ydst, int ndst, void* stream, const void* bias);
 void set_last_cuda_error(int e);
 }  // namespace quick
 
@@ -178,7 +178,7 @@ quick_status_t quick_tp_column_gemm(const void* X, const void* packed, int M, in
     dst[p] = static_cast<__half*>(y_peers[p]) + (size_t)rank * N_local;   // this rank's column slot
   }
   quick_status_t st = quick::gemm_launch(X, packed, M, N_local, K, G, dst[rank], ldy, flags, 0, 0, workspace,
-                                         workspace_bytes, dst, world, stream);
+                                         workspace_bytes, dst, world, stream, nullptr);
   if (st != QUICK_OK) return st;
   return quick_tp::barrier(flag_peers, world, rank, static_cast<cudaStream_t>(stream));
 }
@@ -194,7 +194,7 @@ quick_status_t quick_tp_row_gemm(const void* X_local, const void* packed, int M,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   quick_status_t st = quick::gemm_launch(X_local, packed, M, N, K_local, G, part_peers[rank], N,
                                          flags | QUICK_FLAG_OUT_F32, 0, 0, workspace, workspace_bytes,
-                                         &part_peers[rank], 1, stream);
+                                         &part_peers[rank], 1, stream, nullptr);
   if (st != QUICK_OK) return st;
   // 2 barriers per call: partials ready, then results delivered (partials reusable)
   st = quick_tp::barrier(flag_peers, world, rank, s);

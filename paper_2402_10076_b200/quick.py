@@ -44,6 +44,8 @@ def _load():
         "quick_w4a16_gemm": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
         "quick_w4a16_gemm_ex": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int,
                                         c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
+        "quick_w4a16_gemm_bias": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int,
+                                          c_int, c_int, c_int, c_void_p, c_size_t, c_void_p]),
         "quick_workspace_bytes": (c_size_t, [c_int, c_int, c_int, c_int, c_int, c_int, c_int]),
         "quick_gemm_plan": (c_int, [c_int, c_int, c_int, c_int, c_int, c_size_t, c_void_p, c_void_p, c_void_p,
                                     c_void_p]),
@@ -255,9 +257,10 @@ def workspace_for(shapes, group_size: int, device, *, flags: int = 0):
 # ----------------------------------------------------------------------------- device side
 def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ldy=None, out_fp32=False,
                      pdl=False, no_streamk=False, tile_n: int = 0, split_k: int = 0, workspace=None,
-                     flags: int = 0, stream=None):
-    """Y = X . dequant(Wq) on the GPU.  x: cuda fp16 [M][K]; packed: cuda uint8 blob;
-    workspace: optional zeroed cuda uint8 tensor (quick_workspace_bytes) enabling stream-K plans.
+                     flags: int = 0, stream=None, bias=None):
+    """Y = X . dequant(Wq) (+ bias) on the GPU.  x: cuda fp16 [M][K]; packed: cuda uint8 blob;
+    workspace: optional zeroed cuda uint8 tensor (quick_workspace_bytes) enabling stream-K plans;
+    bias: optional cuda [N] tensor of x's dtype (quick_w4a16_gemm_bias).
     Returns `out` (allocated if None): fp16 [M][N] (fp32 if out_fp32)."""
     import torch
     if x.dtype == torch.bfloat16:          # the bf16 variant: bf16 X, scales (in the blob) and Y
@@ -285,6 +288,15 @@ def quick_w4a16_gemm(x, packed, N: int, K: int, group_size: int, out=None, *, ld
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel()
     fl = flags | (QUICK_FLAG_OUT_F32 if out_fp32 else 0) | (QUICK_FLAG_PDL if pdl else 0) \
         | (QUICK_FLAG_NO_STREAMK if no_streamk else 0)
+    if bias is not None:
+        if not (bias.is_cuda and bias.dtype == x.dtype and bias.is_contiguous() and bias.dim() == 1
+                and bias.numel() == N and bias.device == x.device):
+            raise ValueError(f"bias must be a contiguous cuda {x.dtype} [{N}] tensor")
+        _check("quick_w4a16_gemm_bias", _lib.quick_w4a16_gemm_bias(
+            ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(packed.data_ptr()), ctypes.c_void_p(bias.data_ptr()),
+            M, N, K, group_size, ctypes.c_void_p(out.data_ptr()), ld, fl, tile_n, split_k, ctypes.c_void_p(ws_ptr),
+            ws_bytes, _stream_handle(stream)))
+        return out
     _check("quick_w4a16_gemm_ex", _lib.quick_w4a16_gemm_ex(
         ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(packed.data_ptr()), M, N, K, group_size,
         ctypes.c_void_p(out.data_ptr()), ld, fl, tile_n, split_k, ctypes.c_void_p(ws_ptr), ws_bytes,

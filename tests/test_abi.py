@@ -117,3 +117,19 @@ def test_epilogue_validation():
     d = ctypes.c_void_p(1 << 20)
     assert lib.quick_gather_columns(d, d, 2, 4, 12, null) == quick.QUICK_ERR_UNSUPPORTED
     assert lib.quick_dequant_weights(null, 512, 256, 128, null, null) == quick.QUICK_ERR_INVALID_ARG
+
+
+def test_bias_entry_point_validation():
+    """quick_w4a16_gemm_bias: a null bias is INVALID_ARG; bias with the SiLU epilogue or a misaligned
+    bias is UNSUPPORTED -- all decided on the host before any CUDA call."""
+    lib = quick.raw_library()
+    null = ctypes.c_void_p(0)
+    d = ctypes.c_void_p(1 << 20)
+    args = (8, 256, 512, 128, d, 256)
+    assert lib.quick_w4a16_gemm_bias(d, d, null, *args, 0, 0, 0, null, 0, null) == quick.QUICK_ERR_INVALID_ARG
+    assert lib.quick_w4a16_gemm_bias(d, d, d, *args, quick.QUICK_FLAG_SILU_MUL, 0, 0, null, 0, null) == \
+        quick.QUICK_ERR_UNSUPPORTED
+    assert lib.quick_w4a16_gemm_bias(d, d, ctypes.c_void_p((1 << 20) + 2), *args, 0, 0, 0, null, 0, null) == \
+        quick.QUICK_ERR_UNSUPPORTED
+    assert lib.quick_w4a16_gemm_bias(null, null, d, 0, 256, 512, 128, null, 256, 0, 0, 0, null, 0, null) == \
+        quick.QUICK_OK   # M == 0

@@ -4,6 +4,8 @@ Bars: dequantization bit-exact; GEMM within the north-star toler
 (rel 1e-2, abs 1e-3 where |ref| < 1e-2); bit-exact where the exact result is representable
 (one-hot X, integer-exact regime, zero weights); run-to-run bit-identical.
 """
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -742,3 +744,56 @@ def test_bf16_onehot_bit_exact_and_fp32_out():
     w = oracle.dequant_bf16(p.qweight, p.scales, p.zeros, 128)
     np.testing.assert_array_equal(y.cpu().view(torch.int16).numpy().view(np.uint16), oracle.bf16_bits(w[rows]))
     assert np.max(np.abs(y32.cpu().numpy() - _bf16_ref(p))) < 1e-4
+
+
+# ------------------------------------------------------------------------------- bias epilogue (f2)
+@pytest.mark.parametrize("M,N,K,tile_n,split_k,ws", [(1, 512, 1024, 0, 0, True), (16, 4096, 4096, 0, 0, False),
+                                                     (40, 384, 1024, 32, 3, False), (130, 256, 512, 128, 2, False),
+                                                     (300, 512, 1024, 0, 0, False), (256, 512, 768, 256, 1, False),
+                                                     (7, 28672, 1024, 0, 0, True), (64, 1024, 2048, 64, 0, True)])
+def test_bias_epilogue(M, N, K, tile_n, split_k, ws):
+    """quick_w4a16_gemm_bias over the plan families (whole tile, cluster split-K reduce, stream-K
+    fixed reducer, 256-token tiles, CTA pairs): fp16 Y vs O10 within tolerance, fp32 Y, and bit-exact
+    on the integer-exact set with an integer bias."""
+    p = synth.make_problem(M + 5 * N, M=M, N=N, K=K, G=128)
+    b = (synth.make_x(17, 1, N)[0] * np.float16(0.5)).astype(np.float16)
+    bd = torch.from_numpy(b.view(np.int16)).view(torch.float16).to(DEV)
+    kw = dict(tile_n=tile_n, split_k=split_k, workspace=WS if ws else None)
+    y = quick.quick_w4a16_gemm(to_dev_f16(p.x), pack_dev(p), N, K, 128, bias=bd, **kw)
+    y32 = quick.quick_w4a16_gemm(to_dev_f16(p.x), pack_dev(p), N, K, 128, bias=bd, out_fp32=True, **kw)
+    torch.cuda.synchronize()
+    ref = oracle.add_bias(oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128), b)
+    res = oracle.tol_check(y.float().cpu().numpy(), ref)
+    assert res["ok"], res
+    assert oracle.tol_check(y32.cpu().numpy(), ref)["ok"]
+    pe = synth.make_structured("intexact", 5, M=M, N=N, K=K, G=128)
+    bi = ((np.arange(N) % 9) - 4).astype(np.float16)
+    bid = torch.from_numpy(bi.view(np.int16)).view(torch.float16).to(DEV)
+    ye = quick.quick_w4a16_gemm(to_dev_f16(pe.x), pack_dev(pe), N, K, 128, bias=bid, **kw)
+    refe = oracle.round_fp16(oracle.add_bias(oracle.w4a16_reference(pe.x, pe.qweight, pe.scales, pe.zeros, 128), bi))
+    np.testing.assert_array_equal(f16_bits(ye), refe.view(np.uint16))
+
+
+def test_bias_bf16_and_rejections():
+    """bf16 bias with the bf16 variant (stream-K plan); SiLU + bias and a null bias are rejected."""
+    M, N, K = 24, 512, 1024
+    pb = synth.make_problem_bf16(79, M=M, N=N, K=K, G=128)
+    bb = (0x3F00 + (np.arange(N) % 5) * 0x0010).astype(np.uint16)          # bf16 values in [0.5, 0.62]
+    blob = torch.from_numpy(quick.quick_pack_weights(pb.qweight, pb.scales, pb.zeros, 128)).to(DEV)
+    bdev = torch.from_numpy(bb.view(np.int16)).view(torch.bfloat16).to(DEV)
+    y = quick.quick_w4a16_gemm(_bf16_dev(pb.x), blob, N, K, 128, bias=bdev, workspace=WS)
+    torch.cuda.synchronize()
+    ref = oracle.add_bias(_bf16_ref(pb), oracle.bf16_from_bits(bb))
+    res = oracle.tol_check(y.float().cpu().numpy(), ref)
+    assert res["ok"], res
+    p = synth.make_problem(77, M=M, N=N, K=K, G=128)
+    x, blob16 = to_dev_f16(p.x), pack_dev(p)
+    bd = torch.zeros(N, device=DEV, dtype=torch.float16)
+    with pytest.raises(quick.QuickError):
+        quick.quick_w4a16_gemm(x, blob16, N, K, 128, bias=bd, flags=quick.QUICK_FLAG_SILU_MUL)
+    lib = quick.raw_library()
+    yy = torch.empty((M, N), device=DEV, dtype=torch.float16)
+    null = ctypes.c_void_p(0)
+    st = lib.quick_w4a16_gemm_bias(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(blob16.data_ptr()), null, M, N,
+                                   K, 128, ctypes.c_void_p(yy.data_ptr()), N, 0, 0, 0, null, 0, null)
+    assert st == quick.QUICK_ERR_INVALID_ARG

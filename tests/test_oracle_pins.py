@@ -467,3 +467,29 @@ def test_bf16_gemm_integer_exact_regime():
     y = oracle.gemm_f64(x, w)
     ref = (x.astype(np.int64) @ (codes - zeros[np.arange(K) // G]).astype(np.int64)).astype(np.float64) * 2.0 ** -7
     assert np.array_equal(y, ref)
+
+
+# ------------------------------------------------------------------------------------------ O10
+def test_add_bias_pins():
+    """O10 (R21): zero weights give Y = b exactly; in the integer-exact regime with an
+    integer bias, 64 (Y + b) is the int64 matrix X . (q - z) + 64 b; each row gets the same b;
+    Fraction brute force on a tiny random problem."""
+    pz = synth.make_structured("zero_weights", 4, M=3, N=128, K=256, G=64)
+    b = (np.arange(128) % 17 - 8).astype(np.float16) * np.float16(0.25)
+    y = oracle.add_bias(oracle.w4a16_reference(pz.x, pz.qweight, pz.scales, pz.zeros, 64), b)
+    np.testing.assert_array_equal(y, np.tile(b.astype(np.float64), (3, 1)))
+    p = synth.make_structured("intexact", 5, M=9, N=256, K=512, G=128)
+    bi = ((np.arange(256) % 9) - 4).astype(np.float16)            # integers: exact in fp16
+    q = oracle.unpack_awq(p.qweight).astype(np.int64)
+    z = np.repeat(oracle.unpack_awq(p.zeros).astype(np.int64), 128, axis=0)
+    yint = p.x.astype(np.int64) @ (q - z) + 64 * bi.astype(np.int64)[None, :]
+    y = oracle.add_bias(oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, 128), bi)
+    np.testing.assert_array_equal(y * 64.0, yint.astype(np.float64))
+    pr = synth.make_problem(13, M=2, N=8, K=16, G=8)
+    br = np.array([0.5, -1.25, 3.0, 0.0, -0.0078125, 2.5, 1.0, -3.5], dtype=np.float16)
+    w = oracle.dequant(pr.qweight, pr.scales, pr.zeros, 8)
+    yr = oracle.add_bias(oracle.gemm(pr.x, w), br)
+    for m in range(2):
+        for n in range(8):
+            exact = sum(Fraction(float(pr.x[m, k])) * Fraction(float(w[k, n])) for k in range(16)) + Fraction(float(br[n]))
+            assert abs(Fraction(yr[m, n]) - exact) <= Fraction(1, 2**40)
