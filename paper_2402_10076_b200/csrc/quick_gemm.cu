@@ -96,11 +96,7 @@ struct Cfg {
   // for a 6-7 slot A ring) was measured 1.9x slower per SM than two 2-group CTAs per SM on the
   // 70B shapes at M <= 64 (one MMA warp per SM cannot keep up), so every tile uses 2 groups; the
   // code is written for any power-of-two NPAR.
-#ifdef QUICK_NPAR4
-  static constexpr int NPAR = (SK && BN <= 16) ? 4 : 2;   // probe variant: one 16-warp CTA per SM
-#else
   static constexpr int NPAR = 2;
-#endif
   static constexpr int THREADS = 32 * (4 * NPAR + 2);
   // warp roles: dequant warps 0..4 NPAR - 1, then the producer and the MMA warp.  The build
   // variant QUICK_ROLES_FIRST puts the producer / MMA warps at ids 0 / 1 instead: measured equal
@@ -128,7 +124,7 @@ struct Cfg {
   // released after one A stage instead of two, so more of the ring is in flight -- 28672x8192 and
   // 8192x28672 at M <= 16: 31.1 -> 29.5 us; the cluster split-K tile-16 plans, with few stages
   // per CTA, keep 256-k stages: 4096^2 M = 1 6.4 vs 7.1 us with 128)
-  static constexpr int KL = (BN <= 16 && SK && NPAR == 2) ? 128 : BN <= 32 ? 256 : 128;
+  static constexpr int KL = (BN <= 16 && SK) ? 128 : BN <= 32 ? 256 : 128;
   static constexpr int APL = KL / kKA;              // A stages per load stage
   // tile 128 trades its second CTA per SM for a 4-deep ring (the MMA of a 41 KiB stage takes
   // ~512 cycles, less than the L2/HBM refill latency a 2-deep ring exposes)
