@@ -39,7 +39,12 @@ l2 = torch.cuda.get_device_properties(0).L2_cache_size
 L = 16
 FLAGS = {"auto": 0, "pdl": quick.QUICK_FLAG_PDL, "nosk": quick.QUICK_FLAG_NO_STREAMK,
          "sk": quick.QUICK_FLAG_PDL | (1 << 17),   # debug: stream-K whenever the tile allows it
-         "pdlearly": quick.QUICK_FLAG_PDL | (1 << 24)}
+         "pdlearly": quick.QUICK_FLAG_PDL | (1 << 24),
+         "onecta": quick.QUICK_FLAG_PDL | (1 << 26),   # debug: stream-K with one CTA per SM
+         "exittop": quick.QUICK_FLAG_PDL | (1 << 29),  # debug: return at kernel entry (launch cost)
+         "exitpro": quick.QUICK_FLAG_PDL | (1 << 28),  # debug: return after the prologue
+         "nocomp": quick.QUICK_FLAG_PDL | (1 << 30),   # debug: loads only
+         "nomma": quick.QUICK_FLAG_PDL | (1 << 27)}    # debug: dequant + TMEM stores, no MMA
 
 
 def timeit(launch, reps=5):
