@@ -64,6 +64,8 @@ constexpr int kForcePair = 1 << 20;        // debug: CTA-pair (cta_group::2) pla
 constexpr int kDebugNoPair = 1 << 19;      // debug: automatic plan without CTA pairs
 constexpr int kDebugForceSk = 1 << 17;     // debug: stream-K whenever the tile allows it
 constexpr int kDebugSkReverse = 1 << 16;   // debug: stream-K CTA c takes the unit range of CTA P-1-c
+constexpr int kAblationMmaSync = 1 << 18;  // ablation: M <= 16 stream-K plans on the register-fragment
+                                           // mma.sync decode kernel (QUICK's Ampere design)
 
 // the stream-K "CTA index" that owns unit ranges (blockIdx.x, or reversed under kDebugSkReverse)
 __device__ __forceinline__ int sk_cta(int flags) {
@@ -1540,6 +1542,313 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 }
 
 // ------------------------------------------------------------------------------------------
+// Decode kernel (ablation, opt-in with kAblationMmaSync; M <= 16, stream-K plans): QUICK's
+// register-fragment design, the paper's own (§3, Fig. 4-6), on the warp-level tensor
+// path.  At M <= 16 the tcgen05 kernel spends a quarter of its time storing the dequantized A stage
+// into TMEM (tcgen05.st; without those stores it runs at its loads-only time,
+// profiles/r02b_small_m_tmem_store_probes.txt).  Here the dequantized registers ARE the
+// mma.sync.m16n8k16 A fragment: no TMEM, no MMA warp, no afull/aempty round trip.  Same v1 blob, same
+// stream-K units / workspace / fix-up as the tcgen05 kernel (a 128-row tile, 128-k stages).
+// Measured on B200 (profiles/r02b_decode_mmasync_ab.txt): ~20 % slower than the tcgen05 kernel at
+// 70B M <= 16 -- each thread now issues the HMMAs, its two rows' group constants and the X fragment
+// loads itself (ncu: 25 vs 22 warp instructions per code word, issue slots 63 % busy either way),
+// so the TMEM stores it saves are paid back in issue slots.  The automatic plan keeps tcgen05.
+//
+// Swap-AB: D[n][m] = sum_k W^T[n][k] X^T[k][m], A = 16 weight rows x 16 k (registers), B = 16 k x 8
+// tokens (X from shared memory), D = 16 x 8 fp32 (registers).  Warp w owns rows 16w .. 16w + 15 of
+// the tile; lane = 4g + t holds rows r0 = 16w + g and r1 = r0 + 8.  In the v1 layout word t of a
+// row's 32-k chunk holds k = 32c + 8t + 0..7, and the FT extraction gives the pairs (k0,k1), (k2,k3),
+// (k4,k5), (k6,k7) of that word; the MMA's k index is a free permutation (applied to A and B alike),
+// so MMA step 0 of chunk c takes fragment columns {2t, 2t+1} = k {0, 1} and {2t+8, 2t+9} = k {2, 3},
+// step 1 takes k {4, 5} and {6, 7} -- exactly the thread's own word: one LDS.32 per row and chunk is
+// the A fragment after dequantization, and one LDS.128 of X[token g][32c + 8t .. + 7] (a 16-byte
+// chunk of the same SW128 X tile the tcgen05 kernel uses: conflict-free) is the B fragment of both
+// steps.  NT = 16 tokens adds the second 8-token half (row g + 8 of the X tile).
+template <int NT>
+struct DCfg {
+  static constexpr int WARPS = 8;                    // compute warps (16 rows each)
+  static constexpr int PRODUCER_WARP = WARPS;
+  static constexpr int THREADS = 32 * (WARPS + 1);
+  static constexpr int KL = 128;                     // k per stage (one stream-K unit)
+  static constexpr int CTAS_PER_SM = 2;   // the 16-token stream-K plan's residency (3 per SM measured equal)
+  static constexpr int STAGES = 8;
+  static constexpr int XR = 16;                      // token rows of the X tile (the host's TMA box)
+  static constexpr int X_BYTES = XR * KL * 2;        // [KL/64][16][64] fp16, SWIZZLE_128B
+  static constexpr int X_SUB = XR * 128;
+  static constexpr int W_BYTES = KL * 64;
+  static constexpr int M_BYTES = kMetaBytes;         // one metadata block per stage (G a power of two >= 128)
+  static constexpr int X_OFF = 0;
+  static constexpr int W_OFF = X_OFF + STAGES * X_BYTES;
+  static constexpr int M_OFF = W_OFF + STAGES * W_BYTES;
+  static constexpr int BAR_OFF = (M_OFF + STAGES * M_BYTES + 7) & ~7;
+  static constexpr int NUM_BARS = 3 * STAGES;        // full[STAGES], empty[STAGES], xfull[STAGES]
+  static constexpr int USED = BAR_OFF + NUM_BARS * 8;
+  static constexpr int SMEM_BYTES = USED + 1024;
+  static_assert((SMEM_BYTES + 1024) * CTAS_PER_SM <= 228 * 1024, "decode CTAs per SM");
+  static_assert(NT == 8 || NT == 16, "8 or 16 tokens");
+};
+
+template <bool BF>
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  if constexpr (BF)
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                 "{%8, %9}, {%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+                 "{%8, %9}, {%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int NT, bool BF>
+__global__ void __launch_bounds__(DCfg<NT>::THREADS, DCfg<NT>::CTAS_PER_SM)
+    quick_decode_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ KParams p) {
+  using C = DCfg<NT>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int NH = NT / 8;   // 8-token halves
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = ptx::smem_u32(smem_raw);
+  const uint32_t sbase = (sraw + 1023u) & ~1023u;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int K = p.K, M = p.M;
+  const int C32 = K / 32;
+  const int NG = K / p.G;
+  const int gsh = p.g_shift;   // G a power of two >= 128 (host-checked): one metadata block per stage
+  const bool pdl = (p.flags & QUICK_FLAG_PDL) != 0;
+  const bool silu = false;
+  (void)silu;
+  const uint32_t bar_full = sbase + C::BAR_OFF;
+  const uint32_t bar_empty = bar_full + 8 * STAGES;
+  const uint32_t bar_xfull = bar_empty + 8 * STAGES;
+  if (warp == C::PRODUCER_WARP) {
+    for (int i = lane; i < C::NUM_BARS; i += 32)
+      ptx::mbar_init(bar_full + 8 * i, (i >= STAGES && i < 2 * STAGES) ? (uint32_t)C::WARPS : 1u);
+    ptx::fence_mbar_init();
+    if (lane == 0) ptx::prefetch_tmap(&tmap_x);
+  }
+  __syncthreads();
+  if (p.flags & kDebugPdlEarly) ptx::griddep_launch_dependents();
+
+  if (warp == C::PRODUCER_WARP) {
+    // ------------------------------------------------------------------ producer (one lane issues)
+    const uint64_t pol_w = ptx::policy_evict_first();
+    const uint64_t pol_x = ptx::policy_evict_last();
+    SegIter it(p, true);
+    Seg sg;
+    int slot = 0, lf = 0, pre = -1;
+    uint32_t ph = 0;
+    auto load_x = [&](int xs, int m0, int kc) {
+      ptx::mbar_arrive_expect_tx(bar_xfull + 8 * xs, C::X_BYTES);
+      ptx::tma_load_3d_hint(sbase + C::X_OFF + xs * C::X_BYTES, &tmap_x, 0, m0, kc, bar_xfull + 8 * xs, pol_x);
+    };
+    while (it.next(sg)) {
+      const uint8_t* wbase = p.packed + (size_t)sg.t * C32 * kChunkBytes;
+      const uint8_t* mbase = p.packed + (size_t)K * p.N / 2 + (size_t)sg.t * NG * kMetaBytes;
+      const int m0 = sg.mt * 16;
+      const int k_seg_end = min(sg.a_hi * kKA, K);
+      const int nl = sg.a_hi - sg.a_lo;
+      if (pre < 0) pre = pdl ? (nl < STAGES ? nl : STAGES) : 0;
+      for (int l = 0; l < nl; ++l, ++lf) {
+        const int kl0 = (sg.a_lo + l) * kKA;
+        const int kv = min(kKA, k_seg_end - kl0);
+        if (lf >= pre) ptx::mbar_wait_loop(bar_empty + 8 * slot, ph ^ 1u);
+        const uint32_t full = bar_full + 8 * slot;
+        if (ptx::elect_one()) {
+          ptx::mbar_arrive_expect_tx(full, (uint32_t)kv * 64u + kMetaBytes);
+          ptx::bulk_load_hint(sbase + C::W_OFF + slot * C::W_BYTES, wbase + (size_t)(kl0 / 32) * kChunkBytes,
+                              (uint32_t)kv * 64u, full, pol_w);
+          ptx::bulk_load_hint(sbase + C::M_OFF + slot * C::M_BYTES, mbase + (size_t)(kl0 >> gsh) * kMetaBytes,
+                              kMetaBytes, full, pol_w);
+          if (lf >= pre && !(pre == 0 && lf == 0)) {
+            load_x(slot, m0, kl0 / 64);
+          } else if (lf == (pre > 0 ? pre - 1 : 0)) {
+            if (pdl) ptx::griddep_wait();
+            for (int j = 0; j <= lf; ++j) load_x(j, m0, (sg.a_lo + j) * kKA / 64);
+          }
+        }
+        __syncwarp();
+        if (++slot == STAGES) {
+          slot = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    ptx::griddep_launch_dependents();
+  } else {
+    // ------------------------------------------------------------------ compute warps
+    const int g = lane >> 2, t = lane & 3;
+    const int r0 = 16 * warp + g, r1 = r0 + 8;
+    const uint32_t woff0 = (uint32_t)(r0 * 16 + 4 * t), woff1 = (uint32_t)(r1 * 16 + 4 * t);
+    const uint32_t soff0 = (uint32_t)(2 * r0), soff1 = (uint32_t)(2 * r1);
+    const uint32_t zoff0 = (uint32_t)(256 + (r0 >> 1)), zoff1 = (uint32_t)(256 + (r1 >> 1));
+    const uint32_t zs0 = (uint32_t)(r0 & 1) * 4u, zs1 = (uint32_t)(r1 & 1) * 4u;
+    // X tile: [KL/64][16 rows][64 k], row = 128 B, 16-B chunk j of row g at (j ^ g): chunk c's 16 bytes
+    // for this thread are j = (c & 1) * 4 + t of sub-tile c >> 1 (row g; row g + 8 for the second half)
+    uint32_t xoff[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      xoff[c] = (uint32_t)((c >> 1) * C::X_SUB + g * 128 + ((((c & 1) * 4 + t) ^ g) << 4));
+    auto consts = [&](uint32_t mb, uint32_t soff, uint32_t zoff, uint32_t zs) {
+      const uint32_t zb = ptx::lds_u8(mb + zoff);
+      const uint32_t sbits = ptx::lds_u16(mb + soff);
+      const uint32_t zr = __byte_perm(zb, 0u, 0x4040);
+      DequantConsts c;
+      if constexpr (BF) {
+        c.zlo = ptx::lop3<0xEA>(zr >> zs, 0x000F000Fu, 0x43004300u);
+        c.zhi = 0u;
+      } else {
+        c.zlo = ptx::lop3<0xEA>(zr >> zs, 0x000F000Fu, 0x64006400u);
+        c.zhi = ptx::lop3<0xEA>(zr << (4u - zs), 0x00F000F0u, 0xD400D400u);
+      }
+      c.s2 = __byte_perm(sbits, 0u, 0x1010);
+      return c;
+    };
+    SegIter it(p, true);
+    Seg sg;
+    int slot = 0;
+    uint32_t fph = 0;
+    while (it.next(sg)) {
+      const int k_seg_end = min(sg.a_hi * kKA, K);
+      constexpr int NCH = 2;   // independent accumulation chains (chunk c -> chain c % NCH; 4 measured equal)
+      float acc[NCH][NH][4];
+#pragma unroll
+      for (int i = 0; i < NCH; ++i)
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][h][j] = 0.0f;
+      for (int a = sg.a_lo; a < sg.a_hi; ++a) {
+        const uint32_t fbar = bar_full + 8u * (uint32_t)slot;
+        const uint32_t wb = sbase + C::W_OFF + (uint32_t)slot * C::W_BYTES;
+        const uint32_t mb = sbase + C::M_OFF + (uint32_t)slot * C::M_BYTES;
+        const uint32_t xb = sbase + C::X_OFF + (uint32_t)slot * C::X_BYTES;
+        ptx::mbar_wait_loop(fbar, fph);
+        const DequantConsts c0 = consts(mb, soff0, zoff0, zs0);
+        const DequantConsts c1 = consts(mb, soff1, zoff1, zs1);
+        const bool half = (a * kKA + kKA) > k_seg_end;   // K % 128 == 64: the last stage's chunks 0, 1 only
+        ptx::mbar_wait_loop(bar_xfull + 8u * (uint32_t)slot, fph);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c >= 2 && half) break;
+          const uint32_t w0 = ptx::lds_u32(wb + (uint32_t)(c * kChunkBytes) + woff0);
+          const uint32_t w1 = ptx::lds_u32(wb + (uint32_t)(c * kChunkBytes) + woff1);
+          const uint4 x0 = ptx::lds128(xb + xoff[c]);
+          uint32_t d0[4], d1[4];
+          dequant_w<BF>(w0, c0, d0);
+          dequant_w<BF>(w1, c1, d1);
+          mma16816<BF>(acc[c % NCH][0], d0[0], d1[0], d0[1], d1[1], x0.x, x0.y);
+          mma16816<BF>(acc[c % NCH][0], d0[2], d1[2], d0[3], d1[3], x0.z, x0.w);
+          if constexpr (NH == 2) {
+            const uint4 x1 = ptx::lds128(xb + xoff[c] + 8u * 128u);   // tokens 8 .. 15 (row g + 8)
+            mma16816<BF>(acc[c % NCH][1], d0[0], d1[0], d0[1], d1[1], x1.x, x1.y);
+            mma16816<BF>(acc[c % NCH][1], d0[2], d1[2], d0[3], d1[3], x1.z, x1.w);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(fbar + 8u * STAGES);   // W, metadata and X of this slot consumed
+        if (++slot == STAGES) {
+          slot = 0;
+          fph ^= 1u;
+        }
+      }
+      if (!it.more()) ptx::griddep_launch_dependents();
+      // ---------------------------------------------------------------- segment epilogue
+      // thread (g, t) holds D[row r0 / r1][token 8h + 2t (+1)] = acc[.][h][0..3]
+      float v[NH][4];
+#pragma unroll
+      for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float sum = acc[0][h][j];
+#pragma unroll
+          for (int i = 1; i < NCH; ++i) sum += acc[i][h][j];
+          v[h][j] = sum;
+        }
+      const int n0 = sg.t * kTileRows + r0, n1 = n0 + 8;
+      auto store = [&]() {
+        float b0 = 0.0f, b1 = 0.0f;
+        if (p.bias != nullptr) {
+          b0 = bias_f<BF>(p.bias[n0]);
+          b1 = bias_f<BF>(p.bias[n1]);
+        }
+#pragma unroll 1
+        for (int d = 0; d < p.ndst; ++d) {
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int m = 8 * h + 2 * t + j;
+              if (m < M) {
+                if (p.flags & QUICK_FLAG_OUT_F32) {
+                  float* y = reinterpret_cast<float*>(p.Ydst[d]) + (size_t)m * p.ldy;
+                  y[n0] = v[h][j] + b0;
+                  y[n1] = v[h][2 + j] + b1;
+                } else {
+                  uint16_t* y = reinterpret_cast<uint16_t*>(p.Ydst[d]) + (size_t)m * p.ldy;
+                  y[n0] = cvt16<BF>(v[h][j] + b0);
+                  y[n1] = cvt16<BF>(v[h][2 + j] + b1);
+                }
+              }
+            }
+        }
+      };
+      if (sg.a_lo == 0 && sg.a_hi == p.NA) {
+        store();
+      } else {
+        // stream-K partial tile: the tile's first CTA (c_first, which reaches it at the end of its
+        // range) sums the others' fp32 partials in CTA order; deterministic (as the tcgen05 kernel)
+        const int u_first = sg.tile * p.NA;
+        const int c_first = sk_owner(p, u_first);
+        const int c_last = sk_owner(p, u_first + p.NA - 1);
+        int* sem = p.sems + sg.tile;
+        const int me = sk_cta(p.flags);
+        if (me != c_first) {
+          float* ws = p.ws + (size_t)me * (16 * kTileRows);
+#pragma unroll
+          for (int h = 0; h < NH; ++h)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int m = 8 * h + 2 * t + j;
+              if (m < M) {
+                __stcg(ws + m * kTileRows + r0, v[h][j]);
+                __stcg(ws + m * kTileRows + r1, v[h][2 + j]);
+              }
+            }
+          ptx::named_bar_sync(1, 32 * C::WARPS);
+          if (threadIdx.x == 0) ptx::red_release_gpu_add(sem, 1);
+        } else {
+          if (threadIdx.x == 0) {
+            const int want = c_last - c_first;
+            while (ptx::ld_acquire_gpu(sem) < want) {
+            }
+            *sem = 0;
+          }
+          ptx::named_bar_sync(1, 32 * C::WARPS);
+          for (int cc = c_first + 1; cc <= c_last; ++cc) {
+            const float* ws = p.ws + (size_t)cc * (16 * kTileRows);
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int m = 8 * h + 2 * t + j;
+                if (m < M) {
+                  v[h][j] += __ldcg(ws + m * kTileRows + r0);
+                  v[h][2 + j] += __ldcg(ws + m * kTileRows + r1);
+                }
+              }
+          }
+          store();
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Utility kernels on the same layout.
 // ------------------------------------------------------------------------------------------
 // One thread per 16-byte chunk (t, c, r): 32 codes of column n = 128t + r, k = 32c..32c+31.
@@ -1980,6 +2289,40 @@ cudaError_t set_smem_once(const void* k, int bytes) {
   return e;
 }
 
+// The decode kernel (M <= 16 stream-K plans, quick_decode_kernel): same grid (P CTAs, two per
+// SM), same workspace and units as the 16-token tcgen05 stream-K plan it replaces.
+template <int NT, bool BF>
+quick_status_t launch_decode_t(const CUtensorMap& tmap, quick::KParams& kp, int P, cudaStream_t stream) {
+  using C = quick::DCfg<NT>;
+  auto* k = quick::quick_decode_kernel<NT, BF>;
+  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(k), C::SMEM_BYTES);
+  if (e != cudaSuccess) return cuda_fail(e);
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)P, 1, 1);
+  cfg.blockDim = dim3((unsigned)C::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  int na = 0;
+  if (kp.flags & QUICK_FLAG_PDL) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  kp.trace = nullptr;
+  e = cudaLaunchKernelEx(&cfg, k, tmap, kp);
+  return e == cudaSuccess ? QUICK_OK : cuda_fail(e);
+}
+quick_status_t launch_decode(const CUtensorMap& tmap, quick::KParams& kp, int P, cudaStream_t stream) {
+  const bool bf = (kp.flags & QUICK_FLAG_BF16) != 0;
+  if (kp.M <= 8)
+    return bf ? launch_decode_t<8, true>(tmap, kp, P, stream) : launch_decode_t<8, false>(tmap, kp, P, stream);
+  return bf ? launch_decode_t<16, true>(tmap, kp, P, stream) : launch_decode_t<16, false>(tmap, kp, P, stream);
+}
+
 template <int BN, bool SK>
 quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int P,
                          cudaStream_t stream, bool pair = false) {
@@ -2081,7 +2424,7 @@ constexpr int kKnownFlags = QUICK_FLAG_OUT_F32 | QUICK_FLAG_PDL | QUICK_FLAG_NO_
                             quick::kDebugExitTop | quick::kDebugExitPrologue | quick::kDebugNoMma |
                             quick::kDebugOneCta | quick::kDebugNoSttm | quick::kDebugPdlEarly |
                             quick::kAblationSmemA | quick::kForcePair | quick::kDebugNoPair | quick::kDebugForceSk |
-                            quick::kDebugSkReverse;
+                            quick::kDebugSkReverse | quick::kAblationMmaSync;
 
 // The launch plan of a call: a pure function of the shape, flags and overrides, and of whether
 // a stream-K workspace may be used (`allow_ws`).
@@ -2284,6 +2627,11 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   kp.sk_q = kp.U / max(kp.P, 1);
   kp.sk_r = kp.U - kp.sk_q * max(kp.P, 1);
   if (plan.sk) {
+    // ablation (opt-in): the register-fragment mma.sync decode kernel for M <= 16, G a power of two
+    // >= 128, plain outputs -- measured ~20 % slower than the tcgen05 kernel
+    if ((flags & quick::kAblationMmaSync) && tn == 16 && M <= 16 && kp.g_shift >= 7 && !g_trace &&
+        (flags & QUICK_FLAG_SILU_MUL) == 0)
+      return launch_decode(tmap, kp, plan.P, strm);
     switch (tn) {
       case 16: return launch_bn<16, true>(tmap, kp, 1, plan.P, strm);
       case 32: return launch_bn<32, true>(tmap, kp, 1, plan.P, strm);

@@ -797,3 +797,44 @@ def test_bias_bf16_and_rejections():
     st = lib.quick_w4a16_gemm_bias(ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(blob16.data_ptr()), null, M, N,
                                    K, 128, ctypes.c_void_p(yy.data_ptr()), N, 0, 0, 0, null, 0, null)
     assert st == quick.QUICK_ERR_INVALID_ARG
+
+
+# ------------------------------------------------------------------------------- mma.sync decode ablation
+MMASYNC = 1 << 18   # kAblationMmaSync: the register-fragment decode kernel for M <= 16 stream-K plans
+
+
+@pytest.mark.parametrize("M,N,K,G", [(1, 512, 1024, 128), (5, 384, 1152, 128), (8, 4096, 4096, 128),
+                                     (9, 256, 1152, 128), (16, 1024, 4352, 256), (12, 28672, 1024, 128),
+                                     (16, 640, 2048, 1024)])
+def test_mmasync_decode_ablation(M, N, K, G):
+    """The opt-in register-fragment decode kernel (QUICK's mma.sync design; A fragments straight from
+    the dequantized registers): vs the oracle within tolerance, run-to-run bit-identical (PDL and not),
+    bit-exact on the integer-exact set, with the bias / fp32 epilogues; stream-K segments over tile
+    boundaries and the K % 128 == 64 tail are covered by the shapes."""
+    p = synth.make_problem(M * 11 + K, M=M, N=N, K=K, G=G)
+    x, blob = to_dev_f16(p.x), pack_dev(p)
+    y1 = quick.quick_w4a16_gemm(x, blob, N, K, G, workspace=WS, flags=MMASYNC)
+    y2 = quick.quick_w4a16_gemm(x, blob, N, K, G, workspace=WS, flags=MMASYNC | quick.QUICK_FLAG_PDL)
+    torch.cuda.synchronize()
+    check_tol(p, y1, "mmasync")
+    assert torch.equal(y1.view(torch.int16), y2.view(torch.int16))
+    pe = synth.make_structured("intexact", 5, M=M, N=N, K=K, G=G)
+    ye = quick.quick_w4a16_gemm(to_dev_f16(pe.x), pack_dev(pe), N, K, G, workspace=WS, flags=MMASYNC)
+    ref = oracle.round_fp16(oracle.w4a16_reference(pe.x, pe.qweight, pe.scales, pe.zeros, G))
+    np.testing.assert_array_equal(f16_bits(ye), ref.view(np.uint16))
+    b = (synth.make_x(21, 1, N)[0] * np.float16(0.25)).astype(np.float16)
+    bd = torch.from_numpy(b.view(np.int16)).view(torch.float16).to(DEV)
+    y32 = quick.quick_w4a16_gemm(x, blob, N, K, G, workspace=WS, flags=MMASYNC, bias=bd, out_fp32=True)
+    torch.cuda.synchronize()
+    assert oracle.tol_check(y32.cpu().numpy(), oracle.add_bias(oracle.w4a16_reference(
+        p.x, p.qweight, p.scales, p.zeros, G), b))["ok"]
+
+
+def test_mmasync_decode_ablation_bf16():
+    M, N, K = 7, 512, 1024
+    p = synth.make_problem_bf16(31, M=M, N=N, K=K, G=128)
+    blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, 128)).to(DEV)
+    y = quick.quick_w4a16_gemm(_bf16_dev(p.x), blob, N, K, 128, workspace=WS, flags=MMASYNC)
+    torch.cuda.synchronize()
+    res = oracle.tol_check(y.float().cpu().numpy(), _bf16_ref(p))
+    assert res["ok"], res

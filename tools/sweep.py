@@ -44,7 +44,8 @@ FLAGS = {"auto": 0, "pdl": quick.QUICK_FLAG_PDL, "nosk": quick.QUICK_FLAG_NO_STR
          "exittop": quick.QUICK_FLAG_PDL | (1 << 29),  # debug: return at kernel entry (launch cost)
          "exitpro": quick.QUICK_FLAG_PDL | (1 << 28),  # debug: return after the prologue
          "nocomp": quick.QUICK_FLAG_PDL | (1 << 30),   # debug: loads only
-         "nomma": quick.QUICK_FLAG_PDL | (1 << 27)}    # debug: dequant + TMEM stores, no MMA
+         "nomma": quick.QUICK_FLAG_PDL | (1 << 27),    # debug: dequant + TMEM stores, no MMA
+         "mmasync": quick.QUICK_FLAG_PDL | (1 << 18)}  # ablation: register-fragment mma.sync decode kernel
 
 
 def timeit(launch, reps=5):
