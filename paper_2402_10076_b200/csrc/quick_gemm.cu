@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -188,10 +189,10 @@ struct KParams {
   // (32-bit, no division on the device); partial tiles go through ws and are summed by the
   // last arriver
   int U, P, sk_q, sk_r;
-  // placement-weighted stream-K (sk_wa > 0: CTAs [0, sk_h) take sk_wa / sk_wb times the units of the
-  // others).  Measured on B200 with the first-placed CTA of each SM weighted 1.05-1.2x: slower at every
-  // weight (profiles/r02_sk_placement.txt), so the host always launches uniform ranges (sk_wa = 0)
-  int sk_wa, sk_wb, sk_h;
+  // two-group stream-K (sk_h > 0): CTAs [0, sk_h) own qa units each (+1 for the first ra of them), CTAs
+  // [sk_h, P) qb (+1 for the first rb) -- e.g. less work for the CTA that shares an SM second; all in
+  // 32-bit arithmetic (a 64-bit-division version of this in round 2 made every launch ~4 us slower)
+  int sk_h, sk_qa, sk_ra, sk_qb, sk_rb;
   float* ws;              // [P][BN][128] fp32 partial tile of each CTA's (only) non-reducer segment
   int* sems;              // [tiles] arrival counters, zero between launches (reset by the reducer)
   unsigned long long* trace;
@@ -201,28 +202,22 @@ struct KParams {
 };
 
 __device__ __forceinline__ int sk_start(int c, int q, int r) { return c * q + min(c, r); }
-// first unit of stream-K CTA c (c = P: U), uniform or placement-weighted (KParams::sk_wa)
+// first unit of stream-K CTA c (c = P: U), uniform or two-group (KParams::sk_h)
 __device__ __forceinline__ int sk_begin(const KParams& p, int c) {
-  if (p.sk_wa == 0) return sk_start(c, p.sk_q, p.sk_r);
-  const long long wsum = (long long)p.sk_wa * p.sk_h + (long long)p.sk_wb * (p.P - p.sk_h);
-  const long long cum = c <= p.sk_h ? (long long)p.sk_wa * c
-                                    : (long long)p.sk_wa * p.sk_h + (long long)p.sk_wb * (c - p.sk_h);
-  return (int)(((long long)p.U * cum) / wsum);
+  if (p.sk_h == 0) return sk_start(c, p.sk_q, p.sk_r);
+  if (c <= p.sk_h) return sk_start(c, p.sk_qa, p.sk_ra);
+  return sk_start(p.sk_h, p.sk_qa, p.sk_ra) + sk_start(c - p.sk_h, p.sk_qb, p.sk_rb);
+}
+// the CTA of a uniform run (q units each, +1 for the first r) owning unit u of the run
+__device__ __forceinline__ int sk_owner_run(int u, int q, int r) {
+  const int b = r * (q + 1);
+  return u < b ? u / (q + 1) : r + (u - b) / q;
 }
 // the stream-K CTA owning unit u (the largest c with sk_begin(c) <= u)
 __device__ __forceinline__ int sk_owner(const KParams& p, int u) {
-  if (p.sk_wa == 0) {
-    const int b = p.sk_r * (p.sk_q + 1);
-    return u < b ? u / (p.sk_q + 1) : p.sk_r + (u - b) / p.sk_q;
-  }
-  const long long wsum = (long long)p.sk_wa * p.sk_h + (long long)p.sk_wb * (p.P - p.sk_h);
-  const long long t = ((long long)u * wsum) / p.U;   // ~ cum(c) at unit u
-  const long long ta = (long long)p.sk_wa * p.sk_h;
-  int c = t < ta ? (int)(t / p.sk_wa) : p.sk_h + (int)((t - ta) / p.sk_wb);
-  if (c > p.P - 1) c = p.P - 1;
-  while (c > 0 && sk_begin(p, c) > u) --c;
-  while (c + 1 < p.P && sk_begin(p, c + 1) <= u) ++c;
-  return c;
+  if (p.sk_h == 0) return sk_owner_run(u, p.sk_q, p.sk_r);
+  const int ua = sk_start(p.sk_h, p.sk_qa, p.sk_ra);
+  return u < ua ? sk_owner_run(u, p.sk_qa, p.sk_ra) : p.sk_h + sk_owner_run(u - ua, p.sk_qb, p.sk_rb);
 }
 
 // One contiguous run of A stages [a_lo, a_hi) of one tile (n-tile t, m-tile mt).
@@ -621,6 +616,12 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
             load_x(slot, m0, kl0 / 64);
           } else if (lf == (pre > 0 ? pre - 1 : 0)) {
             if (pdl) ptx::griddep_wait();
+            if (TRACE) {   // (trace records: when the previous grid's completion released this CTA)
+              unsigned long long t_gd;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_gd));
+              const size_t lin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+              p.trace[16 * (size_t)kTraceStride + 4 * lin + 3] = pdl ? t_gd : 0ull;
+            }
             for (int j = 0; j <= lf; ++j)   // X of the stages issued so far (all in this segment)
               load_x(j, m0, (sg.a_lo + j * APL) * kKA / 64);
           }
@@ -1501,13 +1502,13 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
   __syncthreads();
   if (TRACE && tr != nullptr && threadIdx.x == 0 && S == 1 && !SK) tr[6] = clock64();
   if (TRACE && threadIdx.x == 0) {
-    // all CTAs: (smid, start ns, end ns) after the 16 detailed records
+    // all CTAs: (smid, start ns, end ns, griddep release ns) after the 16 detailed records
     unsigned long long t_end_ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end_ns));
     uint32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     const size_t lin = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    unsigned long long* rec = p.trace + 16 * (size_t)kTraceStride + 3 * lin;
+    unsigned long long* rec = p.trace + 16 * (size_t)kTraceStride + 4 * lin;
     rec[0] = smid;
     rec[1] = t_start_ns;
     rec[2] = t_end_ns;
@@ -2626,6 +2627,22 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   kp.P = plan.P;
   kp.sk_q = kp.U / max(kp.P, 1);
   kp.sk_r = kp.U - kp.sk_q * max(kp.P, 1);
+#ifdef QUICK_SK_WEIGHT_PROBE
+  if (plan.sk && plan.P == 2 * sm_count()) {   // probe: CTAs [0, P/2) take QUICK_SK_WEIGHT/1000 x the units
+    static const int wgt = [] { const char* e = getenv("QUICK_SK_WEIGHT"); return e ? atoi(e) : 0; }();
+    if (wgt > 0) {
+      const int h = plan.P / 2;
+      // group A: round(U * w / (w + 1000)) units over h CTAs, group B the rest over P - h
+      const long long ua = ((long long)kp.U * wgt + (wgt + 1000) / 2) / (wgt + 1000);
+      kp.sk_h = h;
+      kp.sk_qa = (int)(ua / h);
+      kp.sk_ra = (int)(ua - (long long)kp.sk_qa * h);
+      kp.sk_qb = (int)((kp.U - ua) / (plan.P - h));
+      kp.sk_rb = (int)((kp.U - ua) - (long long)kp.sk_qb * (plan.P - h));
+      if (kp.sk_qa < 1 || kp.sk_qb < 1) kp.sk_h = 0;
+    }
+  }
+#endif
   if (plan.sk) {
     // ablation (opt-in): the register-fragment mma.sync decode kernel for M <= 16, G a power of two
     // >= 128, plain outputs -- measured ~20 % slower than the tcgen05 kernel

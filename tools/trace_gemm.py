@@ -26,7 +26,7 @@ copies = [blob.clone() for _ in range(max(4, int(3e8 // blob.numel())))]
 x = torch.from_numpy(p.x.view(np.int16)).view(torch.float16).cuda()
 y = torch.empty((M, N), device="cuda", dtype=torch.float16)
 NCTA = _ws.plan(M, N, K, G)["num_ctas"] if not (tn or sk) else 4096
-tr = torch.zeros(16 * STRIDE + 3 * max(NCTA, 4096), dtype=torch.int64, device="cuda")
+tr = torch.zeros(16 * STRIDE + 4 * max(NCTA, 4096), dtype=torch.int64, device="cuda")
 
 
 def run(w):
@@ -42,7 +42,7 @@ torch.cuda.synchronize()
 lib.quick_debug_set_trace(ctypes.c_void_p(0))
 tt = tr.cpu().numpy()
 t = tt[:16 * STRIDE].reshape(16, STRIDE)
-rec = tt[16 * STRIDE:].reshape(-1, 3)
+rec = tt[16 * STRIDE:].reshape(-1, 4)[:, :3]
 rec = rec[rec[:, 1] > 0]
 if len(rec):
     t0 = rec[:, 1].min()
@@ -56,7 +56,7 @@ if len(rec):
     print(f"ALL CTAs: {len(rec)} on {len(per_sm)} SMs, CTAs/SM histogram {cnt.tolist()}, kernel span {span:.2f} us, "
           f"CTA duration min/med/max {dur.min():.2f}/{np.median(dur):.2f}/{dur.max():.2f} us, SM finish min/med/max "
           f"{busy.min():.2f}/{np.median(busy):.2f}/{busy.max():.2f} us, start skew max {(rec[:,1].max()-t0)/1e3:.2f} us")
-    full = tt[16 * STRIDE:].reshape(-1, 3)
+    full = tt[16 * STRIDE:].reshape(-1, 4)
     idx = np.nonzero(full[:, 1] > 0)[0]
     # per SM: the CTAs sharing it, by launch index (is the same one always the fast one?)
     by_sm = {}
