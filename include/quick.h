@@ -135,7 +135,9 @@ size_t quick_workspace_bytes(int M, int N, int K, int group_size, int flags, int
  *             choose stream-K for tiles <= 64)
  *   workspace, workspace_bytes
  *             caller-owned device memory, 256-byte aligned, ZEROED by the caller once before
- *             its first use (every launch leaves it zeroed again).  The stream-K plan is used
+ *             its first use: its first 256 KiB hold the stream-K arrival counters, which every
+ *             launch leaves zeroed again (the rest is scratch for fp32 partial tiles), so one
+ *             workspace may serve calls of any shapes in sequence.  The stream-K plan is used
  *             only if workspace_bytes >= quick_workspace_bytes(...) of this call; otherwise
  *             the workspace-free plan runs (so the plan never depends on anything but the
  *             arguments).  NULL / 0 = no workspace.  Two launches that may run concurrently

@@ -2153,11 +2153,16 @@ int max_resident_pair(int bn, int S) {
 
 // ---------------------------------------------------------------------------------------
 // Stream-K workspace: CALLER-OWNED (quick_workspace_bytes / the workspace arguments of
-// quick_w4a16_gemm_ex).  Layout: [tiles] int32 arrival counters (zero between launches: the
-// caller zeroes the buffer once, every launch leaves them zero), padded to 256 B, then the
-// [P][BN][128] fp32 partial tiles.  The library never allocates, frees or synchronises.
+// quick_w4a16_gemm_ex).  Layout: 65536 int32 arrival counters (256 KiB, zero between launches: the
+// caller zeroes the buffer once, every launch leaves them zero), then the [P][BN][128] fp32 partial
+// tiles (scratch).  The library never allocates, frees or synchronises.
 constexpr size_t kSemAlign = 256;
-size_t sk_sem_bytes(long long tiles) { return (((size_t)tiles * sizeof(int)) + kSemAlign - 1) / kSemAlign * kSemAlign; }
+// The counter region has a FIXED size (kMaxSkTiles counters, 256 KiB), so that calls of different
+// shapes sharing one workspace never see another call's fp32 partials where their counters live
+// (round 2 sized it by the call's own tile count: a call with fewer tiles wrote partials over the
+// counters of a later call with more tiles).
+constexpr long long kMaxSkTiles = 65536;
+size_t sk_sem_bytes(long long /*tiles*/) { return (size_t)kMaxSkTiles * sizeof(int); }
 size_t sk_ws_bytes(long long tiles, int P, int bn) {
   return sk_sem_bytes(tiles) + (size_t)P * bn * quick::kTileRows * sizeof(float);
 }
@@ -2192,7 +2197,8 @@ Plan choose_plan(int M, int N, int K, int G, int force_tile, int force_split, bo
   const int NA = (K + quick::kKA - 1) / quick::kKA;
   const int tn = force_tile > 0 ? force_tile : cover_tile(M);
   const int tiles = (N / quick::kTileRows) * ((M + tn - 1) / tn);
-  if (allow_sk && force_split == 0 && sk_capable(tn) && (long long)tiles * NA < (1LL << 30)) {
+  if (allow_sk && force_split == 0 && sk_capable(tn) && (long long)tiles * NA < (1LL << 30) &&
+      tiles <= kMaxSkTiles) {
     const long long U = (long long)tiles * NA;
     const long long resident = (long long)max_resident(tn, true, 1);
     long long P = std::min(resident, std::max(1LL, U / 4));

@@ -838,3 +838,20 @@ def test_mmasync_decode_ablation_bf16():
     torch.cuda.synchronize()
     res = oracle.tol_check(y.float().cpu().numpy(), _bf16_ref(p))
     assert res["ok"], res
+
+
+def test_workspace_shared_across_shapes_counters_stay_zero():
+    """One zeroed workspace serving stream-K calls of different shapes in sequence (tile counts going
+    up and down): every result within tolerance and the 256 KiB counter region zero after each call.
+    (Round 2 sized the counter region by the call's own tile count, so a call with few tiles left
+    fp32 partials where a later call with more tiles kept its counters.)"""
+    ws = torch.zeros(24 << 20, dtype=torch.uint8, device=DEV)
+    shapes = [(16, 512, 2048), (16, 28672, 1024), (16, 384, 4096), (1, 28672, 2048), (7, 256, 8192),
+              (16, 13824, 2048), (3, 1024, 1024)]
+    for i, (M, N, K) in enumerate(shapes):
+        p = synth.make_problem(300 + i, M=M, N=N, K=K, G=128)
+        plan = quick.quick_gemm_plan(M, N, K, 128, workspace_bytes=ws.numel())
+        y = quick.quick_w4a16_gemm(to_dev_f16(p.x), pack_dev(p), N, K, 128, workspace=ws, pdl=True)
+        torch.cuda.synchronize()
+        check_tol(p, y, (M, N, K, plan))
+        assert int(torch.count_nonzero(ws[:256 << 10])) == 0, (M, N, K, plan)

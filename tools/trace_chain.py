@@ -36,10 +36,17 @@ s = torch.cuda.current_stream().cuda_stream
 for w in range(3):   # warm-up (untraced)
     _ws.gemm_raw(x.data_ptr(), copies[w].data_ptr(), M, N, K, G, y.data_ptr(), s, quick.QUICK_FLAG_PDL | XF, TN, SK)
 torch.cuda.synchronize()
-for i in range(L):
-    lib.quick_debug_set_trace(ctypes.c_void_p(bufs[i].data_ptr()))
-    _ws.gemm_raw(x.data_ptr(), copies[3 + i].data_ptr(), M, N, K, G, y.data_ptr(), s, quick.QUICK_FLAG_PDL | XF, TN, SK)
+# the traced launches are captured in one CUDA graph (eager launches of short kernels are host-bound:
+# the GPU would idle between them), each with its own trace buffer
+stream = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=stream):
+    for i in range(L):
+        lib.quick_debug_set_trace(ctypes.c_void_p(bufs[i].data_ptr()))
+        _ws.gemm_raw(x.data_ptr(), copies[3 + i].data_ptr(), M, N, K, G, y.data_ptr(), stream.cuda_stream,
+                     quick.QUICK_FLAG_PDL | XF, TN, SK)
 lib.quick_debug_set_trace(ctypes.c_void_p(0))
+g.replay()
 torch.cuda.synchronize()
 print("plan", plan, "launches", L)
 prev_end = None
