@@ -855,3 +855,43 @@ def test_workspace_shared_across_shapes_counters_stay_zero():
         torch.cuda.synchronize()
         check_tol(p, y, (M, N, K, plan))
         assert int(torch.count_nonzero(ws[:256 << 10])) == 0, (M, N, K, plan)
+
+
+def test_randomized_shapes_and_plans_against_oracle():
+    """Seeded random sweep over the supported shape space (N % 128, K % 64, G in {32, 64, 128, 256, K}),
+    token counts 1 .. 300, automatic / stream-K / forced plans, PDL on and off, fp16 and bf16 -- each
+    against the oracle; a cheap net for plan and tail edge cases the hand-picked cases miss."""
+    rng = np.random.default_rng(2402)
+    for case in range(40):
+        G = int(rng.choice([32, 64, 128, 256]))
+        K = int(G * rng.integers(1, max(2, 2560 // G)))
+        if K % 64:
+            K += 64 - K % 64
+            if K % G:
+                G = 64 if K % 64 == 0 else 32
+        N = int(128 * rng.integers(1, 12))
+        M = int(rng.choice([1, 2, 3, 8, 15, 16, 17, 31, 33, 64, 65, 127, 128, 129, 200, 256, 300]))
+        mode = int(rng.integers(0, 4))
+        kw = {}
+        if mode == 1:
+            kw["workspace"] = WS
+        elif mode == 2:
+            kw["tile_n"] = int(rng.choice([16, 32, 64, 128, 256]))
+            kw["split_k"] = int(rng.integers(1, min(8, (K + 127) // 128) + 1))
+        elif mode == 3:
+            kw["workspace"] = WS
+            kw["pdl"] = True
+        bf = bool(rng.integers(0, 5) == 0)
+        if bf:
+            p = synth.make_problem_bf16(1000 + case, M=M, N=N, K=K, G=G)
+            blob = torch.from_numpy(quick.quick_pack_weights(p.qweight, p.scales, p.zeros, G)).to(DEV)
+            y = quick.quick_w4a16_gemm(_bf16_dev(p.x), blob, N, K, G, **kw)
+            torch.cuda.synchronize()
+            res = oracle.tol_check(y.float().cpu().numpy(), _bf16_ref(p))
+        else:
+            p = synth.make_problem(1000 + case, M=M, N=N, K=K, G=G)
+            y = quick.quick_w4a16_gemm(to_dev_f16(p.x), pack_dev(p), N, K, G, **kw)
+            torch.cuda.synchronize()
+            res = oracle.tol_check(y.float().cpu().numpy(),
+                                   oracle.w4a16_reference(p.x, p.qweight, p.scales, p.zeros, G))
+        assert res["ok"], (case, M, N, K, G, kw, bf, res)
