@@ -128,10 +128,14 @@ class ColumnParallelW4A16:
         gathered = self._gathered[M]
         y = out if out is not None else t.empty((M, self.N), device=self.device, dtype=t.float16)
         local = gathered[self.rank]                     # compute straight into our slot
-        self.quick.quick_w4a16_gemm(x, self.packed, self.Nr, self.K, self.G, out=local, workspace=self.workspace)
+        nvtx = t.cuda.nvtx   # (ranges for nsys / ncu --nvtx; no cost without a profiler)
+        with nvtx.range("quick.column.gemm"):
+            self.quick.quick_w4a16_gemm(x, self.packed, self.Nr, self.K, self.G, out=local, workspace=self.workspace)
         # in-place all-gather: the input is this rank's slice of the output buffer
-        self.dist.all_gather_into_tensor(gathered.view(-1), local.view(-1), group=self.group)
-        self.quick.quick_gather_columns(gathered, self.world, M, self.Nr, dst=y)
+        with nvtx.range("quick.column.all_gather"):
+            self.dist.all_gather_into_tensor(gathered.view(-1), local.view(-1), group=self.group)
+        with nvtx.range("quick.column.gather_columns"):
+            self.quick.quick_gather_columns(gathered, self.world, M, self.Nr, dst=y)
         return y
 
 
@@ -167,10 +171,14 @@ class RowParallelW4A16:
         if M not in self._partial:
             self._partial[M] = t.empty((M, self.N), device=self.device, dtype=t.float32)
         partial = self._partial[M]
-        self.quick.quick_w4a16_gemm(x_shard, self.packed, self.N, self.Kr, self.G, out=partial, out_fp32=True,
-                                    workspace=self.workspace)
-        self.dist.all_reduce(partial, op=self.dist.ReduceOp.SUM, group=self.group)   # fp32 on the wire
-        self.quick.quick_f32_to_f16(partial, dst=y)
+        nvtx = t.cuda.nvtx
+        with nvtx.range("quick.row.gemm_fp32"):
+            self.quick.quick_w4a16_gemm(x_shard, self.packed, self.N, self.Kr, self.G, out=partial, out_fp32=True,
+                                        workspace=self.workspace)
+        with nvtx.range("quick.row.all_reduce_fp32"):
+            self.dist.all_reduce(partial, op=self.dist.ReduceOp.SUM, group=self.group)   # fp32 on the wire
+        with nvtx.range("quick.row.to_fp16"):
+            self.quick.quick_f32_to_f16(partial, dst=y)
         return y
 
 
