@@ -183,6 +183,10 @@ struct KParams {
   void* Ydst[kMaxPeers];
   int M, N, K, G, g_shift, ldy, flags;
   int n_tiles, m_tiles;   // tile index = t * m_tiles + mt (n-tile major: a CTA's tiles share weights)
+  // cluster grids (not stream-K): gridDim.y = m_grp m-tiles, gridDim.z = n_cl n-tile clusters (n-tiles, or
+  // n-tile pairs) x m_tiles / m_grp groups -- all n-tiles of one m-tile group run before the next group, so
+  // a long-K X (70B down, M = 1024: 58.7 MB) is resident in L2 one group at a time
+  int m_grp, n_cl;
   int NA;                 // A stages (128 k) per tile: ceil(K / 128)
   // stream-K (gridDim = (P, 1, 1)): the U = tiles x NA (tile, A stage) units are cut into P
   // contiguous ranges, U = P q + r: CTA c owns [c q + min(c, r), ...) of q + (c < r) units
@@ -247,8 +251,10 @@ struct SegIter {
     } else {
       const int S = pair ? (int)gridDim.x >> 1 : (int)gridDim.x;
       const int sp = pair ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
-      t = pair ? 2 * (int)blockIdx.z + ((int)blockIdx.x & 1) : (int)blockIdx.z;
-      mt = blockIdx.y;
+      const int grp = (int)blockIdx.z / p.n_cl;
+      const int zc = (int)blockIdx.z - grp * p.n_cl;
+      t = pair ? 2 * zc + ((int)blockIdx.x & 1) : zc;
+      mt = grp * p.m_grp + (int)blockIdx.y;
       a_lo = (sp * NA) / S;          // 32-bit: S <= 8 and NA = ceil(K / 128) < 2^27
       a_hi = ((sp + 1) * NA) / S;
       u = u1 = 0;
@@ -1370,7 +1376,9 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[5] = clock64();
     ptx::cluster_sync();
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[6] = clock64();
-    const int m0 = blockIdx.y * BN;
+    const int grp = (int)blockIdx.z / p.n_cl;
+    const int zc = (int)blockIdx.z - grp * p.n_cl;
+    const int m0 = (grp * p.m_grp + (int)blockIdx.y) * BN;
     const uint32_t my = PAIR ? (crank >> 1) : ptx::cluster_ctarank();   // split index
     constexpr int E4 = BN * kTileRows / 4;   // the tile in float4 units, split evenly over S
     const int eb = (int)(((int)my * E4) / S) * 4;
@@ -1380,7 +1388,7 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
 #pragma unroll
     for (int q = 0; q < kMaxSplit; ++q)   // (pair: the same member of each split's pair)
       peer[q] = ptx::mapa(sbase, PAIR ? (uint32_t)(2 * (q < S ? q : 0)) + member : (uint32_t)(q < S ? q : 0));
-    const int tt = PAIR ? 2 * (int)blockIdx.z + (int)member : (int)blockIdx.z;
+    const int tt = PAIR ? 2 * zc + (int)member : zc;
     // partial q of element e (float4 index): our own through ld.shared, the others' through DSMEM
     auto load_part = [&](int q, int e) {
       if (q == (int)my) {
@@ -2341,7 +2349,8 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
   if (SK)
     cfg.gridDim = dim3((unsigned)P, 1, 1);
   else
-    cfg.gridDim = dim3((unsigned)S, (unsigned)kp.m_tiles, (unsigned)kp.n_tiles);   // m-tiles adjacent
+    cfg.gridDim = dim3((unsigned)S, (unsigned)kp.m_grp,   // m-tiles of a group adjacent, groups outermost
+                       (unsigned)(kp.n_tiles * (kp.m_tiles / kp.m_grp)));
   cfg.blockDim = dim3((unsigned)C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   if (kp.flags & quick::kDebugOneCta) cfg.dynamicSmemBytes = std::max<size_t>(C::SMEM_BYTES, 120 * 1024);
@@ -2378,7 +2387,7 @@ quick_status_t launch_bn(const CUtensorMap& tmap, quick::KParams& kp, int S, int
                                             : quick::quick_w4a16_tc_kernel<BN, false, false, false, 2>);
       e = set_smem_once(reinterpret_cast<const void*>(kq), CP::SMEM_BYTES);
       if (e != cudaSuccess) return cuda_fail(e);
-      cfg.gridDim = dim3((unsigned)(2 * S), (unsigned)kp.m_tiles, (unsigned)(kp.n_tiles / 2));
+      cfg.gridDim = dim3((unsigned)(2 * S), (unsigned)kp.m_grp, (unsigned)(kp.n_tiles / 2 * (kp.m_tiles / kp.m_grp)));
       cfg.dynamicSmemBytes = CP::SMEM_BYTES;
       cfg.blockDim = dim3((unsigned)CP::THREADS, 1, 1);
       na = 0;
@@ -2586,6 +2595,18 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
     }
   }
   kp.m_tiles = (M + plan.tile_n - 1) / plan.tile_n;
+  // m-tile groups (cluster grids): the largest divisor of m_tiles whose X rows (m_grp x tile_n x K fp16)
+  // stay within 40 MB of L2 next to the streamed weights; a single group otherwise
+  kp.m_grp = kp.m_tiles;
+  if (!plan.sk) {
+    const long long x_tile = (long long)plan.tile_n * K * 2;
+    while (kp.m_grp > 1 && (long long)kp.m_grp * x_tile > (40LL << 20)) {
+      int d = kp.m_grp - 1;
+      while (d > 1 && kp.m_tiles % d != 0) --d;
+      kp.m_grp = d;
+    }
+  }
+  kp.n_cl = plan.pair ? kp.n_tiles / 2 : kp.n_tiles;
   const int tn = plan.tile_n, s = plan.split;
 
   // X viewed as [K/64][M][64] (dims innermost first: k within a 64-chunk, token, k-chunk): one

@@ -435,7 +435,8 @@ def test_pair_bit_identical_and_oracle(M, N, K, tn, sk, G):
 
 
 @pytest.mark.parametrize("M,N,K", [(1024, 28672, 8192), (256, 13824, 5120), (512, 4096, 4096), (128, 8192, 28672),
-                                   (256, 4096, 4096)])   # the last: the configs[1] bench's dominant launch
+                                   (256, 4096, 4096),    # the configs[1] bench's dominant launch
+                                   (1024, 8192, 28672)])  # m-tile groups (X > 40 MB): two groups of 4 m-tiles
 def test_pair_auto_plan_full_size_pdl(M, N, K):
     """The automatic plan picks CTA pairs for these large-M shapes; launched as a PDL chain in a CUDA
     graph (the bench's mode) the result is bit-identical to ordinary launches of the same plan, and
