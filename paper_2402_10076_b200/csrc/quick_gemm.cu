@@ -1502,8 +1502,14 @@ __global__ void __launch_bounds__(Cfg<BN, SK, AM>::THREADS, Cfg<BN, SK, AM>::MAX
     }
     if (TRACE && tr != nullptr && threadIdx.x == 0) tr[7] = clock64();
     // peers may still be reading our partials: arrive now (our own DSMEM reads are done), wait
-    // only at the very end, so the barrier latency overlaps the teardown
-    ptx::cluster_arrive();
+    // only at the very end, so the barrier latency overlaps the teardown.  Relaxed: the barrier only
+    // keeps our shared memory alive for the peers' reads (every value we loaded from theirs has been
+    // consumed by the sums above); nothing written before it must become visible to them (4096^2:
+    // M = 16 6.80 -> 6.54 us, M = 128 10.74 -> 10.23 us, profiles/r02c_relaxed_arrive_ab.txt).
+    // (A push variant -- each CTA cp.async.bulk-copies the other owners' token chunks of its partial
+    // into their shared memory, completing on an mbarrier, then sums locally -- was slower at every
+    // cluster-split point, e.g. 4096^2 M = 128 11.69 vs 10.36 us: profiles/r02c_push_reduce_negative.txt)
+    ptx::cluster_arrive_relaxed();
   }
 
   ptx::tc_fence_before();
