@@ -529,78 +529,92 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective, 
     xd = [g["xs"][0] for g in gemms]
     sh = stream.cuda_stream
 
-    def gemm_call(gi, g, slot):
+    def gemm_call(gi, g, slot, x=None, y=None, w=None, s=None):
         fl = (quick.QUICK_FLAG_OUT_F32 if g["y"].dtype == torch.float32 else 0) | \
             (quick.QUICK_FLAG_SILU_MUL if g["kind"] == "silu" else 0)
-        quick.quick_w4a16_gemm_raw(xd[gi].data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nl"], g["Kl"],
-                                   G, g["y"].data_ptr(), sh, flags=fl, ws_ptr=ws.data_ptr(), ws_bytes=ws.numel(),
-                                   ldy=g["n_out"])
+        x = xd[gi] if x is None else x
+        y = g["y"] if y is None else y
+        w = ws if w is None else w
+        quick.quick_w4a16_gemm_raw(x.data_ptr(), wcopies[g["si"]][slot].data_ptr(), g["M"], g["Nl"], g["Kl"],
+                                   G, y.data_ptr(), sh if s is None else s, flags=fl, ws_ptr=w.data_ptr(),
+                                   ws_bytes=w.numel(), ldy=g["n_out"])
 
     pipelined = world == 1
-    if pipelined:
-        # copies overlap the GEMMs, as a serving loop would run them: X uploads on one copy
-        # stream, Y downloads on another, the GEMMs on `stream`; per-GEMM buffers and events
-        # order each GEMM after its upload and each download after its GEMM, and an upload /
-        # GEMM waits for the previous step's use of its buffer
-        s_h2d, s_d2h = torch.cuda.Stream(stream.device), torch.cuda.Stream(stream.device)
-        ev = {k: [torch.cuda.Event() for _ in gemms] for k in ("h2d", "comp", "d2h")}
-        started = [False] * len(gemms)
-
-    def step(i):
-        for gi, g in enumerate(gemms):
-            slot = (i * len(gemms) + gi) % R
-            if not pipelined:
+    graphs, replay_streams = [], []
+    if not pipelined:
+        def step(i):
+            for gi, g in enumerate(gemms):
+                slot = (i * len(gemms) + gi) % R
                 xd[gi].copy_(xh[gi], non_blocking=True)
                 gemm_call(gi, g, slot)
                 collective(g)
                 yh[gi].copy_(out_of[gi], non_blocking=True)
-                continue
-            with torch.cuda.stream(s_h2d):
-                if started[gi]:
-                    s_h2d.wait_event(ev["comp"][gi])      # the previous GEMM on xd[gi] is done
-                xd[gi].copy_(xh[gi], non_blocking=True)
-                ev["h2d"][gi].record(s_h2d)
-            stream.wait_event(ev["h2d"][gi])
-            if started[gi]:
-                stream.wait_event(ev["d2h"][gi])          # y[gi] has been read back
-            gemm_call(gi, g, slot)
-            ev["comp"][gi].record(stream)
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev["comp"][gi])
-                yh[gi].copy_(out_of[gi], non_blocking=True)
-                ev["d2h"][gi].record(s_d2h)
-            started[gi] = True
-
-    for i in range(3):
-        step(i)
-    torch.cuda.synchronize()
-    graph = None
-    if pipelined:
-        # one step = one CUDA-graph replay: the uploads, GEMMs (C-ABI calls, captured) and
-        # read-backs with their cross-stream event edges, forked from and joined to `stream`
-        # (replays on `stream` are ordered, so buffers are reused safely across steps)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            fork = torch.cuda.Event()
-            fork.record(stream)
-            s_h2d.wait_event(fork)
-            s_d2h.wait_event(fork)
-            started[:] = [False] * len(gemms)
-            step(0)
-            for gi in range(len(gemms)):
-                stream.wait_event(ev["d2h"][gi])
-            stream.wait_event(ev["h2d"][len(gemms) - 1])
-        graph.replay()
+        for i in range(3):
+            step(i)
         torch.cuda.synchronize()
+    else:
+        # Copies overlap the GEMMs, as a serving loop would run them: each step is one CUDA-graph replay
+        # holding the X uploads (one copy stream), the captured C-ABI GEMM calls and the Y read-backs
+        # (another copy stream) with per-GEMM event edges.  Two such graphs over two independent sets of
+        # device buffers, workspaces and host read-back buffers are replayed alternately on two streams,
+        # so step i + 1's uploads run while step i's last GEMMs and read-backs finish (PCIe is the bound
+        # of this workload: 148 MB each way per step); a graph waits only for its own previous replay.
+        s_h2d, s_d2h = torch.cuda.Stream(stream.device), torch.cuda.Stream(stream.device)
+        for si in range(2):
+            if si == 0:
+                xs_, ys_, ws_, yh_ = xd, [g["y"] for g in gemms], ws, yh
+            else:
+                xs_ = [torch.empty_like(x) for x in xd]
+                ys_ = [torch.empty_like(g["y"]) for g in gemms]
+                ws_ = torch.zeros_like(ws)   # a concurrent replay must not share the stream-K counters
+                yh_ = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in out_of]
+            rs = torch.cuda.Stream(stream.device)
+            ev = {k: [torch.cuda.Event() for _ in gemms] for k in ("h2d", "comp")}
+            for gi, g in enumerate(gemms):   # eager warm-up of this set's calls
+                gemm_call(gi, g, gi % R, xs_[gi], ys_[gi], ws_, rs.cuda_stream)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=rs):
+                fork = torch.cuda.Event()
+                fork.record(rs)
+                s_h2d.wait_event(fork)
+                s_d2h.wait_event(fork)
+                for gi, g in enumerate(gemms):
+                    with torch.cuda.stream(s_h2d):
+                        xs_[gi].copy_(xh[gi], non_blocking=True)
+                        ev["h2d"][gi].record(s_h2d)
+                    rs.wait_event(ev["h2d"][gi])
+                    gemm_call(gi, g, (si * len(gemms) + gi) % R, xs_[gi], ys_[gi], ws_, rs.cuda_stream)
+                    ev["comp"][gi].record(rs)
+                    with torch.cuda.stream(s_d2h):
+                        s_d2h.wait_event(ev["comp"][gi])
+                        yh_[gi].copy_(ys_[gi], non_blocking=True)
+                join_h, join_d = torch.cuda.Event(), torch.cuda.Event()
+                join_h.record(s_h2d)
+                join_d.record(s_d2h)
+                rs.wait_event(join_h)
+                rs.wait_event(join_d)
+            graph.replay()
+            torch.cuda.synchronize()
+            graphs.append(graph)
+            replay_streams.append(rs)
     if dist is not None:
         dist.barrier()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for i in range(steps):
-        if graph is not None:
-            graph.replay()
-        else:
+    if graphs:
+        for rs in replay_streams:
+            rs.wait_event(a)
+        for i in range(steps):
+            with torch.cuda.stream(replay_streams[i % 2]):
+                graphs[i % 2].replay()
+        for rs in replay_streams:
+            done = torch.cuda.Event()
+            done.record(rs)
+            stream.wait_event(done)
+    else:
+        for i in range(steps):
             step(i)
     b.record(stream)
     torch.cuda.synchronize()
@@ -616,7 +630,9 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective, 
             "steps": steps, "ms_per_step": round(ms / steps, 4),
             "path": ("C-ABI quick_w4a16_gemm_ex per GEMM (caller-owned workspace), pinned H2D X + D2H Y each step"
                      + ("; one CUDA-graph replay per step holding the uploads, the captured C-ABI GEMM calls and "
-                        "the read-backs on three streams with event dependencies (copies overlap GEMMs)"
+                        "the read-backs on three streams with event dependencies (copies overlap GEMMs); two such "
+                        "graphs over independent buffer sets replayed alternately on two streams (step i+1's "
+                        "uploads overlap step i's tail)"
                         if world == 1 else "; eager, with the TP collectives and epilogue kernels"))}
 
 
