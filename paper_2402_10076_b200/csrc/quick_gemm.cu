@@ -2655,6 +2655,17 @@ quick_status_t gemm_launch(const void* X, const void* packed, int M, int N, int 
   // B200: 28672x8192 M = 1 31.1 -> 30.4 us).  Grids smaller than the machine keep the late trigger
   // (an early one lets the next grid double up on busy SMs).
   if (plan.sk && (kp.flags & QUICK_FLAG_PDL) && plan.P >= max_resident(tn, true, 1)) kp.flags |= quick::kDebugPdlEarly;
+  // Cluster split-K plans of the 16/32-token tiles with at most one CTA per SM and short CTAs (<= 8 A
+  // stages) trigger early too: the grid is mostly its ramp and split-K reduce, so the next GEMM's
+  // prologue and weight prefetch gain from starting on the idle SMs and under the reduce (4096^2 M = 1
+  // 6.42 -> 6.24 us, M = 32 7.56 -> 7.13).  With long CTAs the early CTAs' weight streams slow the
+  // running grid (4096x14336, 28 stages per CTA: 12.2 -> 15.0 us); the 64-token tile loses as well
+  // (4096^2 8.50 -> 9.16 us): profiles/r02c_pdl_early_cluster_ab.txt
+#ifndef QUICK_NO_EARLY_CLUSTER
+  if (!plan.sk && !plan.pair && tn <= 32 && plan.ctas <= sm_count() && (NA + plan.split - 1) / plan.split <= 8 &&
+      (kp.flags & QUICK_FLAG_PDL))
+    kp.flags |= quick::kDebugPdlEarly;
+#endif
   kp.NA = NA;
   kp.U = kp.n_tiles * kp.m_tiles * NA;   // < 2^31: checked by choose_plan
   kp.P = plan.P;
