@@ -600,19 +600,35 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective, 
             replay_streams.append(rs)
     if dist is not None:
         dist.barrier()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    if graphs:
-        for rs in replay_streams:
+    def replay_steps(n, sets):
+        # n steps; `sets` graphs alternate (1: every step on graph 0's stream, serialised)
+        for rs in replay_streams[:sets]:
             rs.wait_event(a)
-        for i in range(steps):
-            with torch.cuda.stream(replay_streams[i % 2]):
-                graphs[i % 2].replay()
-        for rs in replay_streams:
+        for i in range(n):
+            with torch.cuda.stream(replay_streams[i % sets]):
+                graphs[i % sets].replay()
+        for rs in replay_streams[:sets]:
             done = torch.cuda.Event()
             done.record(rs)
             stream.wait_event(done)
+
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    sets, trial = 1, {}
+    if graphs:
+        # warm-up trial of both modes: the two-graph overlap wins when PCIe bounds the step (70B: 4.1 ->
+        # 3.4 ms) but loses when the step is many small GEMMs that the two graphs then run concurrently
+        # (4096^2: 86 -> 53 TFLOP/s); the faster one is timed
+        for m in (1, 2):
+            a.record(stream)
+            replay_steps(4, m)
+            b.record(stream)
+            torch.cuda.synchronize()
+            trial[m] = a.elapsed_time(b)
+        sets = min(trial, key=trial.get)
+    a.record(stream)
+    if graphs:
+        replay_steps(steps, sets)
     else:
         for i in range(steps):
             step(i)
@@ -628,11 +644,14 @@ def run_e2e(args, gemms, wcopies, R, G, stream, dist, world, quick, collective, 
             "h2d_bytes_per_step": int(sum(x.numel() * 2 for x in xh)),
             "d2h_bytes_per_step": int(sum(y.numel() * y.element_size() for y in yh)),
             "steps": steps, "ms_per_step": round(ms / steps, 4),
+            **({"trial_ms_per_step": {("one graph" if m == 1 else "two graphs"): round(t / 4, 4) for m, t in trial.items()}}
+               if graphs else {}),
             "path": ("C-ABI quick_w4a16_gemm_ex per GEMM (caller-owned workspace), pinned H2D X + D2H Y each step"
                      + ("; one CUDA-graph replay per step holding the uploads, the captured C-ABI GEMM calls and "
-                        "the read-backs on three streams with event dependencies (copies overlap GEMMs); two such "
-                        "graphs over independent buffer sets replayed alternately on two streams (step i+1's "
-                        "uploads overlap step i's tail)"
+                        "the read-backs on three streams with event dependencies (copies overlap GEMMs)"
+                        + ("; two such graphs over independent buffer sets replayed alternately on two streams "
+                           "(step i+1's uploads overlap step i's tail)" if sets == 2 else
+                           "; consecutive replays of one graph (faster than two alternating graphs here)")
                         if world == 1 else "; eager, with the TP collectives and epilogue kernels"))}
 
 
