@@ -255,8 +255,8 @@ def test_full_size_shapes_sampled(M, N, K):
 
 
 # ------------------------------------------------------------------------------- PDL
-@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (16, 13824, 5120), (16, 28672, 1024), (64, 4096, 4096),
-                                   (200, 4096, 4096), (256, 2048, 4096)])
+@pytest.mark.parametrize("M,N,K", [(1, 4096, 4096), (32, 4096, 4096), (16, 6144, 4096), (16, 13824, 5120),
+                                   (16, 28672, 1024), (64, 4096, 4096), (200, 4096, 4096), (256, 2048, 4096)])
 def test_pdl_chain_matches_ordinary_launches(M, N, K):
     """QUICK_FLAG_PDL (the bench's launch mode): the second GEMM reads the first one's output as
     its X and is launched programmatically dependent on it, so its weight prefetch and first
